@@ -1,0 +1,173 @@
+// ks_internal.cuh -- device-side data structures and helpers shared by the
+// K-sort engine's kernels (fast mode, exact mode, heap sort, utilities).
+//
+// Vocabulary follows the reference (sort_core.py): a *segment* is a subrange
+// a[left..right] awaiting partition (the reference's worklist entry,
+// sort_core.py:182-198); its *key* is its first element (sort_core.py:82);
+// values with key <= v route right (sort_core.py:90).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include <climits>
+
+#include "../../include/ksort.h"
+
+namespace ks {
+
+// ---------------------------------------------------------------------------
+// Fast-mode tunables.
+// ---------------------------------------------------------------------------
+constexpr int kPMax = 511;            // max pivot candidates (first P keys) per global pass
+constexpr int kPMaxPow2 = 512;
+constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs
+constexpr int kLutMax = 1024;         // LUT buckets (pow2 >= 2*kPMax)
+constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
+constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
+constexpr int kPassThreads = 512;     // threads of count/scatter CTAs
+constexpr int kLeafMax = 8192;        // S: segments <= S finish on chip (one CTA)
+constexpr int kLeafThreads = 512;
+constexpr int kGapsPerLeaf = 4;       // P ~ 4*len/S so that gaps average S/8
+
+constexpr unsigned long long kNoIndex = ~0ull;
+
+// phase ids (ks_status_t.phase_*)
+enum Phase : int { kPhGate = 0, kPhPivots = 1, kPhCount = 2, kPhScan = 3, kPhScatter = 4, kPhPlan = 5,
+                   kPhLeaf = 6, kPhOther = 7 };
+
+__device__ __forceinline__ void add_bytes(struct DevStatus *st, int phase, unsigned long long b);
+
+// Device-resident status / counters of one sort call (lives in the workspace).
+struct DevStatus {
+    unsigned long long bad_index;     // min non-finite index (atomicMin), kNoIndex if none
+    unsigned int pos_zero;            // saw +0.0
+    unsigned int neg_zero;            // saw -0.0
+    int nseg[2];                      // segment counts of the two level tables
+    int nleaf;                        // leaf descriptors of the current level
+    int nchunks;                      // chunks of the current level
+    long long mat_total;              // count-matrix entries of the current level
+    int overflow;                     // a capacity bound was exceeded (bug guard)
+    int pad;
+    unsigned long long bytes_moved;   // algorithmic bytes, all passes
+    unsigned long long phase_bytes[8];  // per phase (ksort.h KS_FLAG_PROFILE numbering)
+    unsigned long long keys_partitioned;
+    unsigned long long keys_leaf;
+    unsigned long long leaves;
+    unsigned long long comparisons;   // exact mode op counts
+    unsigned long long moves;
+};
+
+// One active segment of a global partition pass.
+struct Seg {
+    long long start;   // absolute index of the segment's first key (its K-sort key)
+    long long len;
+    long long mat_off; // first count-matrix entry (class-major rows x nch columns)
+    int P;             // pivot candidates: the first P keys of the segment
+    int k;             // distinct pivots among them
+    int rows;          // 2P+1 matrix rows
+    int nch;           // chunks (columns)
+    int ch_off;        // first global chunk id
+    int piv_off;       // offset into the pivot pool (P slots)
+    int lut_off;       // offset into the LUT pool (T+1 slots)
+    int T;             // LUT buckets (1 = plain binary search)
+    double lo, scale;  // LUT transform t = clamp((v - lo) * scale, 0, T-1)
+};
+
+// Work item of the on-chip finishing pass.
+enum LeafKind : int { kLeafSort = 0, kLeafFill = 1, kLeafCopy = 2 };
+struct Leaf {
+    long long start;
+    long long len;
+    double value;      // fill value (the pivot of an equality run)
+    int kind;
+    int src;           // 0: keys hold the data, 1: tmp holds the data
+};
+
+__device__ __forceinline__ void add_bytes(DevStatus *st, int phase, unsigned long long b)
+{
+    if (b == 0) return;
+    atomicAdd(&st->phase_bytes[phase], b);
+    atomicAdd(&st->bytes_moved, b);
+}
+
+__device__ __forceinline__ bool abort_requested(const DevStatus *st)
+{
+    // Non-finite key (sort_core.py:178) or both signed zeros present (the
+    // fast engine's output is bit-exact only when equal keys are bitwise equal).
+    return st->bad_index != kNoIndex || (st->pos_zero && st->neg_zero);
+}
+
+// Monotone LUT bucket of v: t(v) non-decreasing in v.  (v - lo) and the product
+// round monotonically; scale is finite and > 0 whenever T > 1 (guarded on the
+// host side of the table build), so no NaN can arise from finite v.
+__device__ __forceinline__ int lut_bucket(double v, double lo, double scale, int T)
+{
+    if (T <= 1) return 0;
+    double x = (v - lo) * scale;
+    x = fmin(fmax(x, 0.0), (double)(T - 1));
+    return (int)x;
+}
+
+// Class of v against sorted distinct pivots piv[0..k):
+//   lower = #pivots < v;  class = 2*lower + (v == piv[lower]).
+// Even classes are gaps (open value intervals between pivots, i.e. the
+// unfinished subtrees of the K-sort tree), odd classes are equality runs
+// (the pivot and its copies: K-sort routes them right of the key, where they
+// are already final).  lut[t]..lut[t+1] brackets lower for bucket t.
+__device__ __forceinline__ int classify(double v, const double *piv, int k, const int *lut,
+                                        double lo, double scale, int T)
+{
+    int t = lut_bucket(v, lo, scale, T);
+    int a = lut[t], b = lut[t + 1];
+    while (a < b) {
+        int mid = (a + b) >> 1;
+        if (piv[mid] < v) a = mid + 1; else b = mid;
+    }
+    int eq = (a < k && piv[a] == v) ? 1 : 0;
+    return 2 * a + eq;
+}
+
+__host__ __device__ __forceinline__ long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+__host__ __device__ __forceinline__ int next_pow2(int x)
+{
+    int p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// Block-wide exclusive scan of one long long per thread (blockDim.x <= 1024,
+// multiple of 32).  `sh` needs 33 slots.  Returns the exclusive prefix and the
+// block total through *total.
+__device__ __forceinline__ long long block_exclusive_scan(long long x, long long *sh, long long *total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        long long w = lane < nw ? sh[lane] : 0;
+        long long winc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            long long y = __shfl_up_sync(0xffffffffu, winc, o);
+            if (lane >= o) winc += y;
+        }
+        if (lane < nw) sh[lane] = winc - w;   // exclusive warp offsets
+        if (lane == 31) sh[32] = winc;        // lanes >= nw add 0: lane 31 holds the total
+    }
+    __syncthreads();
+    long long res = sh[wid] + inc - x;
+    if (total) *total = sh[32];
+    __syncthreads();
+    return res;
+}
+
+}  // namespace ks

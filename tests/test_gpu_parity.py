@@ -1,0 +1,405 @@
+"""Parity of the sm_100a engine against the reference (GPU; run with -m gpu).
+
+Oracle: fixtures produced by the reference itself (tests/golden/*.json, made
+by tests/golden/make_golden.py) and the C restatement in oracle/ (pinned to
+those fixtures by tests/test_oracle.py).  Comparisons are BYTEWISE
+(float64 bit patterns), never ``==``, so -0.0/+0.0 arrangements count.
+Mirrors the reference's own hot-path tests (pkg/tests/test_sort_core.py,
+test_acceptance.py C1/C2) through the drop-in API.
+"""
+import itertools
+import math
+import random
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1107_3622_b200 as K  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from tests.golden_io import load, same_bits, sha256, unhex  # noqa: E402
+
+TRACE_ARRAY = [55.0, 66.0, 60.0, 78.0, 22.0, 50.0, 75.0, 5.0, 8.0, 94.0]
+TRACE_SORTED = [5.0, 8.0, 22.0, 50.0, 55.0, 60.0, 66.0, 75.0, 78.0, 94.0]
+
+
+def dev(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def oracle_ksort(a):
+    b = np.array(a, dtype=np.float64, copy=True)
+    O.k_sort(b)
+    return b
+
+
+# ---- golden trace / partition (exact engine) --------------------------------------
+
+def test_partition_golden_calls_1_to_3():
+    # reference tests/test_sort_core.py:31-54, test_acceptance.py:63-69
+    a = list(TRACE_ARRAY)
+    out = K.ksort_partition(a, 0, 9)
+    assert a == [8.0, 5.0, 50.0, 22.0, 55.0, 66.0, 75.0, 78.0, 60.0, 94.0]
+    assert out.pivot_index == 4 and out.flag_used and a[5] == 66.0
+    out = K.ksort_partition(a, 0, 3)
+    assert a == [5.0, 8.0, 50.0, 22.0, 55.0, 66.0, 75.0, 78.0, 60.0, 94.0]
+    assert out.pivot_index == 1 and out.flag_used and a[2] == 50.0
+    out = K.ksort_partition(a, 2, 3)
+    assert a == [5.0, 8.0, 22.0, 50.0, 55.0, 66.0, 75.0, 78.0, 60.0, 94.0]
+    assert out.pivot_index == 3 and not out.flag_used
+
+
+def test_partition_fixtures_bitwise():
+    for case in load("partition.json"):
+        a = dev(unhex(case["input"]))
+        c = K.OpCounts()
+        out = K.ksort_partition(a, case["left"], case["right"], c)
+        assert same_bits(host(a), unhex(case["output"])), case
+        assert out.pivot_index == case["pivot"] and out.flag_used == case["flag"]
+        assert c.comparisons == case["counts"]["comparisons"]
+        assert c.moves == case["counts"]["moves"]
+
+
+def test_partition_edge_cases():
+    a = [3.0, 3.0, 3.0, 3.0]
+    assert K.ksort_partition(a, 0, 3).pivot_index == 0 and a == [3.0] * 4
+    a = [2.0, 1.0]
+    out = K.ksort_partition(a, 0, 1)
+    assert a == [1.0, 2.0] and out.pivot_index == 1 and not out.flag_used
+    b = [1.0, 2.0]
+    out = K.ksort_partition(b, 0, 1)
+    assert b == [1.0, 2.0] and out.pivot_index == 0 and out.flag_used
+    for left, right in ((0, 0), (2, 1), (-1, 2), (0, 3), (3, 4)):
+        with pytest.raises(ValueError):
+            K.ksort_partition([1.0, 2.0, 3.0], left, right)
+    with pytest.raises(K.NonFiniteKeyError):
+        K.ksort_partition([1.0, float("nan"), 3.0], 0, 2)
+    # NaN outside the segment is not inspected (sort_core.py:161)
+    a = [float("nan"), 2.0, 1.0]
+    K.ksort_partition(a, 1, 2)
+    assert a[1:] == [1.0, 2.0]
+
+
+def test_partition_large_segment_matches_oracle():
+    rng = np.random.default_rng(3)
+    for n, left, right in ((5000, 0, 4999), (100_000, 17, 99_000), (70_000, 5, 69_990)):
+        a = np.floor(rng.random(n) * 50) / 7.0
+        b = a.copy()
+        piv, flag, c = O.partition(b, left, right, counts=True)
+        t = dev(a)
+        cc = K.OpCounts()
+        out = K.ksort_partition(t, left, right, cc)
+        assert same_bits(host(t), b)
+        assert (out.pivot_index, out.flag_used) == (piv, flag)
+        assert (cc.comparisons, cc.moves) == (c.comparisons, c.moves)
+
+
+# ---- full sorts against reference outputs --------------------------------------------
+
+def test_sort_fixtures_ksort_bitwise():
+    for case in load("sorts.json"):
+        a = dev(unhex(case["input"]))
+        K.k_sort(a)
+        assert same_bits(host(a), unhex(case["ksort"])), case["input"][:8]
+
+
+def test_sort_fixtures_counts():
+    for case in load("sorts.json"):
+        a = dev(unhex(case["input"]))
+        c = K.OpCounts()
+        K.k_sort(a, c)
+        assert same_bits(host(a), unhex(case["ksort"]))
+        assert c.__dict__ == case["ksort_counts"], case["input"][:8]
+
+
+def test_sort_fixtures_heapsort():
+    for case in load("sorts.json"):
+        a = dev(unhex(case["input"]))
+        K.heap_sort(a)
+        assert same_bits(host(a), unhex(case["heapsort"]))
+        a = dev(unhex(case["input"]))
+        c = K.OpCounts()
+        K.heap_sort(a, c)
+        assert same_bits(host(a), unhex(case["heapsort"]))
+        want = dict(case["heapsort_counts"])
+        assert c.__dict__ == want
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_large_fixtures(idx):
+    case = load("large.json")[idx]
+    n, seed, kind = case["n"], case["seed"], case["kind"]
+    if kind in ("uniform01", "dup256"):
+        a = K.generate_device(n, seed, kind)
+    elif kind == "constant":
+        a = torch.full((n,), 0.5, dtype=torch.float64, device="cuda")
+    else:
+        a = dev(np.sort(O.uniform01(seed, n)))
+        if kind == "sorted_descending":
+            a = a.flip(0).contiguous()
+    assert sha256(host(a)) == case["input_sha256"]
+    b = a.clone()
+    K.k_sort(a)
+    assert sha256(host(a)) == case["ksort_sha256"]
+    c = K.OpCounts()
+    K.k_sort(b, c)
+    assert sha256(host(b)) == case["ksort_sha256"]
+    assert c.__dict__ == case["ksort_counts"]
+
+
+def test_golden_trace_counts():
+    # reference tests/test_sort_core.py:129-137 (20 comparisons, 26 moves, 2 pending)
+    a = list(TRACE_ARRAY)
+    c = K.OpCounts()
+    K.k_sort(a, c)
+    assert a == TRACE_SORTED
+    assert (c.comparisons, c.moves, c.max_pending_ranges) == (20, 26, 2)
+
+
+# ---- the reference's correctness suite (test_sort_core.py:223-275, C2) ---------------
+
+@pytest.mark.parametrize("sorter", ["ksort", "heapsort"])
+def test_exhaustive_small_permutations(sorter):
+    f = K.SORTERS[sorter]
+    for n in range(1, 8):
+        expect = [float(v) for v in range(1, n + 1)]
+        perms = list(itertools.permutations(expect))
+        if n <= 5:
+            for perm in perms:
+                a = list(perm)
+                f(a)
+                assert a == expect
+        # all perms of this n through the batch API in one launch
+        flat = torch.tensor([x for p in perms for x in p], dtype=torch.float64, device="cuda")
+        off = torch.arange(0, len(perms) * n + 1, n, dtype=torch.int64, device="cuda")
+        K.k_sort_segments(flat, off)
+        assert same_bits(host(flat), np.tile(np.array(expect), len(perms)))
+
+
+def test_exhaustive_binary_arrays():
+    for n in range(1, 8):
+        arrs = list(itertools.product((0.0, 1.0), repeat=n))
+        flat = torch.tensor([x for p in arrs for x in p], dtype=torch.float64, device="cuda")
+        off = torch.arange(0, len(arrs) * n + 1, n, dtype=torch.int64, device="cuda")
+        K.k_sort_segments(flat, off)
+        want = np.concatenate([np.sort(np.array(p)) for p in arrs])
+        assert same_bits(host(flat), want)
+        for p in arrs[:: max(1, len(arrs) // 16)]:
+            a = list(p)
+            K.k_sort(a)
+            assert a == sorted(p)
+
+
+def test_random_arrays_vs_oracle():
+    # acceptance C2 (test_acceptance.py:108-124): seed 20260816, n <= 4096
+    rng = random.Random(20260816)
+    for _ in range(300):
+        n = rng.randint(0, 4096)
+        base = [rng.random() for _ in range(n)]
+        a = dev(base)
+        K.k_sort(a)
+        assert same_bits(host(a), oracle_ksort(base))
+
+
+def test_random_finite_doubles_incl_signed_zeros():
+    # hypothesis-style (test_sort_core.py:253-275): arbitrary finite doubles,
+    # including subnormals, extremes and mixed -0.0/+0.0
+    rng = np.random.default_rng(7)
+    specials = np.array([0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, -1.7976931348623157e308,
+                         1.7976931348623157e308, 1.0, -1.0])
+    for t in range(200):
+        n = int(rng.integers(0, 300))
+        bits = rng.integers(0, 2**64, size=n, dtype=np.uint64).view(np.float64)
+        bits = np.where(np.isfinite(bits), bits, 0.0)
+        mask = rng.random(n) < 0.3
+        bits[mask] = rng.choice(specials, size=int(mask.sum()))
+        a = dev(bits)
+        K.k_sort(a)
+        assert same_bits(host(a), oracle_ksort(bits)), t
+        h = bits.copy()
+        O.heap_sort(h)
+        b = dev(bits)
+        K.heap_sort(b)
+        assert same_bits(host(b), h), t
+
+
+# ---- errors and trivial inputs ------------------------------------------------------
+
+def test_trivial_inputs():
+    for a in ([], [1.0], [2.0, 1.0], [1.0, 2.0]):
+        b = list(a)
+        K.k_sort(b)
+        assert b == sorted(a)
+        c = list(a)
+        K.heap_sort(c)
+        assert c == sorted(a)
+
+
+@pytest.mark.parametrize("n", [3, 5000, 8192, 8193, 100_000, 2_000_000])
+def test_nonfinite_rejected_before_any_write(n):
+    rng = np.random.default_rng(n)
+    for bad in (float("nan"), float("inf"), float("-inf")):
+        base = rng.random(n)
+        pos = int(rng.integers(0, n))
+        base[pos] = bad
+        base[n - 1] = bad
+        a = dev(base)
+        before = host(a).copy()
+        with pytest.raises(K.NonFiniteKeyError) as ei:
+            K.k_sort(a)
+        assert str(ei.value) == f"key at index {min(pos, n - 1)} is {bad!r}; keys must be finite"
+        assert same_bits(host(a), before)
+        with pytest.raises(K.NonFiniteKeyError):
+            K.heap_sort(a)
+        assert same_bits(host(a), before)
+    with pytest.raises(K.NonFiniteKeyError):
+        K.k_sort([float("nan")])
+
+
+def test_list_and_numpy_and_cpu_tensor_inputs():
+    rng = np.random.default_rng(1)
+    base = rng.random(20000)
+    want = np.sort(base)
+    a = base.tolist()
+    K.k_sort(a)
+    assert same_bits(np.array(a), want)
+    b = base.copy()
+    K.k_sort(b)
+    assert same_bits(b, want)
+    c = torch.from_numpy(base.copy())
+    K.k_sort(c)
+    assert same_bits(c.numpy(), want)
+    assert K.is_sorted(a) and K.is_sorted(c) and not K.is_sorted(base)
+
+
+# ---- adversarial shapes (forward progress + parity) ----------------------------------
+
+@pytest.mark.parametrize("kind", ["presorted", "reversed", "constant", "organ", "few_distinct"])
+@pytest.mark.parametrize("n", [2048, 8193, 60_000])
+def test_adversarial_inputs(kind, n):
+    rng = np.random.default_rng(n)
+    if kind == "presorted":
+        a = np.arange(n, dtype=np.float64)
+    elif kind == "reversed":
+        a = np.arange(n, 0, -1, dtype=np.float64)
+    elif kind == "constant":
+        a = np.full(n, 0.5)
+    elif kind == "organ":
+        a = np.concatenate([np.arange(n // 2), np.arange(n - n // 2, 0, -1)]).astype(np.float64)
+    else:
+        a = rng.integers(0, 3, size=n).astype(np.float64)
+    t = dev(a)
+    K.k_sort(t)
+    assert same_bits(host(t), np.sort(a))
+
+
+def test_worklist_depth_bound():
+    # test_sort_core.py:163-177
+    rng = random.Random(41)
+    cases = [[rng.random() for _ in range(1000)], [rng.random() for _ in range(4096)],
+             [float(v) for v in range(2048)], [float(v) for v in range(2048, 0, -1)], [0.5] * 1024]
+    for a in cases:
+        n = len(a)
+        want = O.k_sort(np.array(a), counts=True)
+        c = K.OpCounts()
+        K.k_sort(a, c)
+        assert K.is_sorted(a)
+        assert c.max_pending_ranges <= math.ceil(math.log2(n)) + 1
+        assert c.__dict__ == want.__dict__
+
+
+# ---- BASELINE.json configs at full size ----------------------------------------------
+
+@pytest.mark.parametrize("n,kind", [(100_000, "uniform01"), (1_000_000, "uniform01"), (7_000_000, "uniform01"),
+                                    (10_000_000, "uniform01"), (10_000_000, "dup256")])
+def test_configs_full_size_bitexact(n, kind):
+    seed = 20260816
+    a = K.generate_device(n, seed, kind)
+    K.k_sort(a)
+    ref = O.uniform01(seed, n) if kind == "uniform01" else O.dup256(seed, n)
+    # no -0.0 in these workloads: np.sort's bytes are the reference K-sort's
+    # bytes (any correct sort of keys whose equal values are bitwise equal)
+    assert np.signbit(ref).sum() == 0
+    assert same_bits(host(a), np.sort(ref))
+    assert K.last_stats.bytes_moved > 0
+
+
+def test_config_1e5_against_oracle_ksort_and_heap():
+    seed = 20260816
+    base = O.uniform01(seed, 100_000)
+    a = K.generate_device(100_000, seed)
+    K.k_sort(a)
+    assert same_bits(host(a), oracle_ksort(base))
+    h = base.copy()
+    O.heap_sort(h)
+    b = K.generate_device(100_000, seed)
+    K.heap_sort(b)
+    assert same_bits(host(b), h)
+
+
+def test_batch_config_500x100k():
+    seed = 20260816
+    m, nseg = 100_000, 500
+    parts = [O.uniform01(O.derive_seed(seed, r, 0), m) for r in range(nseg)]
+    flat = dev(np.concatenate(parts))
+    off = torch.arange(0, m * nseg + 1, m, dtype=torch.int64, device="cuda")
+    K.k_sort_segments(flat, off)
+    got = host(flat)
+    for r in range(nseg):
+        assert same_bits(got[r * m:(r + 1) * m], np.sort(parts[r])), r
+
+
+def test_batch_ragged_segments():
+    rng = np.random.default_rng(11)
+    sizes = [0, 1, 2, 3, 8192, 8193, 17, 0, 40_000, 1, 5, 123_457, 9000, 2]
+    data = [np.floor(rng.random(s) * 97) / 13.0 for s in sizes]
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    flat = dev(np.concatenate(data))
+    K.k_sort_segments(flat, torch.from_numpy(off).cuda())
+    got = host(flat)
+    for i, d in enumerate(data):
+        assert same_bits(got[off[i]:off[i + 1]], oracle_ksort(d)), i
+
+
+def test_batch_signed_zeros_uses_exact_engine():
+    rng = np.random.default_rng(5)
+    segs = [rng.choice([0.0, -0.0, 0.5, -0.25], size=s) for s in (50, 9000, 3)]
+    off = np.concatenate([[0], np.cumsum([len(s) for s in segs])]).astype(np.int64)
+    flat = dev(np.concatenate(segs))
+    K.k_sort_segments(flat, torch.from_numpy(off).cuda())
+    got = host(flat)
+    for i, s in enumerate(segs):
+        assert same_bits(got[off[i]:off[i + 1]], oracle_ksort(s))
+
+
+def test_signed_zero_large_input_exact_engine():
+    rng = np.random.default_rng(9)
+    a = rng.choice([0.0, -0.0, 1.0, -1.0, 0.5], size=30_000)
+    t = dev(a)
+    K.k_sort(t)
+    assert same_bits(host(t), oracle_ksort(a))
+    assert K.last_stats.exact_used
+
+
+def test_device_generator_matches_reference_stream():
+    for seed in (0, 7, 20260816):
+        assert same_bits(host(K.generate_device(4097, seed)), O.uniform01(seed, 4097))
+        assert same_bits(host(K.generate_device(4097, seed, "dup256")), O.dup256(seed, 4097))
+
+
+def test_sizes_around_thresholds():
+    rng = np.random.default_rng(2)
+    for n in (8191, 8192, 8193, 16384, 16385, 32769, 65536 * 2 + 3, 300_001):
+        a = rng.random(n)
+        t = dev(a)
+        K.k_sort(t)
+        assert same_bits(host(t), np.sort(a)), n
