@@ -22,14 +22,18 @@ namespace ks {
 // ---------------------------------------------------------------------------
 constexpr int kPMax = 511;            // max pivot candidates (first P keys) per global pass
 constexpr int kPMaxPow2 = 512;
-constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs
-constexpr int kLutMax = 1024;         // LUT buckets (pow2 >= 2*kPMax)
+constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (1023)
+constexpr int kLutMax = 2048;         // LUT buckets (pow2 >= 4*P)
+constexpr int kKeysPerPivot = 64;     // P = len / 64 (capped): gaps average ~64..200 keys
 constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
-constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
-constexpr int kPassThreads = 512;     // threads of count/scatter CTAs
-constexpr int kLeafMax = 8192;        // S: segments <= S finish on chip (one CTA)
-constexpr int kLeafThreads = 512;
-constexpr int kGapsPerLeaf = 4;       // P ~ 4*len/S so that gaps average S/8
+constexpr int kCountThreads = 512;
+constexpr int kTile = 8192;           // keys staged in shared memory per scatter step
+constexpr int kPassThreads = 512;     // threads of scatter CTAs (16 keys each per tile)
+constexpr int kLeafMax = 8192;        // S: gaps <= S finish on chip
+constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
+constexpr int kFillMin = 32;          // equality runs >= this are filled, not scattered
+constexpr int kBigThreads = 512;      // CTA of the big-gap sorter
+constexpr int kUnitWarps = 8;         // warps per CTA of the unit sorter
 
 constexpr unsigned long long kNoIndex = ~0ull;
 
@@ -45,7 +49,8 @@ struct DevStatus {
     unsigned int pos_zero;            // saw +0.0
     unsigned int neg_zero;            // saw -0.0
     int nseg[2];                      // segment counts of the two level tables
-    int nleaf;                        // leaf descriptors of the current level
+    int nunits;                       // warp work items (unit sorts, fills) of the current pass
+    int nbig;                         // CTA work items (gaps of kUnitMax+1 .. S keys)
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
@@ -69,20 +74,25 @@ struct Seg {
     int rows;          // 2P+1 matrix rows
     int nch;           // chunks (columns)
     int ch_off;        // first global chunk id
-    int piv_off;       // offset into the pivot pool (P slots)
-    int lut_off;       // offset into the LUT pool (T+1 slots)
+    int piv_off;       // offset into the pivot pool (P+1 slots: +inf sentinel)
+    int lut_off;       // offset into the LUT pool (T int2 slots)
     int T;             // LUT buckets (1 = plain binary search)
+    int pad0, pad1;
     double lo, scale;  // LUT transform t = clamp((v - lo) * scale, 0, T-1)
 };
 
 // Work item of the on-chip finishing pass.
-enum LeafKind : int { kLeafSort = 0, kLeafFill = 1, kLeafCopy = 2 };
-struct Leaf {
+//  unit: <= kUnitMax keys (a gap plus its pivot's equality run) sorted by one warp
+//  fill: an equality run written with the pivot value, no read
+//  big:  a gap of kUnitMax+1 .. S keys sorted by one CTA
+enum ItemKind : int { kItemUnit = 0, kItemFill = 1, kItemBig = 2 };
+struct Item {
     long long start;
-    long long len;
-    double value;      // fill value (the pivot of an equality run)
-    int kind;
+    int len;
+    int kind;          // ItemKind
     int src;           // 0: keys hold the data, 1: tmp holds the data
+    int pad;
+    double value;      // fill value (the pivot of an equality run)
 };
 
 __device__ __forceinline__ void add_bytes(DevStatus *st, int phase, unsigned long long b)
@@ -110,23 +120,32 @@ __device__ __forceinline__ int lut_bucket(double v, double lo, double scale, int
     return (int)x;
 }
 
-// Class of v against sorted distinct pivots piv[0..k):
+// Class of v against sorted distinct pivots piv[0..k) (piv[k] = NaN sentinel):
 //   lower = #pivots < v;  class = 2*lower + (v == piv[lower]).
 // Even classes are gaps (open value intervals between pivots, i.e. the
 // unfinished subtrees of the K-sort tree), odd classes are equality runs
 // (the pivot and its copies: K-sort routes them right of the key, where they
-// are already final).  lut[t]..lut[t+1] brackets lower for bucket t.
-__device__ __forceinline__ int classify(double v, const double *piv, int k, const int *lut,
-                                        double lo, double scale, int T)
+// are already final).  lut[t] = (#pivots in buckets < t, #pivots in buckets <= t)
+// brackets lower for bucket t; two predicated probes resolve it in the common
+// case, a binary search handles crowded buckets.
+__device__ __forceinline__ int classify(double v, const double *piv, const int2 *lut, double lo, double scale,
+                                        int T)
 {
-    int t = lut_bucket(v, lo, scale, T);
-    int a = lut[t], b = lut[t + 1];
-    while (a < b) {
-        int mid = (a + b) >> 1;
-        if (piv[mid] < v) a = mid + 1; else b = mid;
+    const int t = lut_bucket(v, lo, scale, T);
+    const int2 ab = lut[t];
+    int a = ab.x;
+    const int b = ab.y;
+    a += (a < b && piv[a] < v) ? 1 : 0;
+    a += (a < b && piv[a] < v) ? 1 : 0;
+    if (a < b && piv[a] < v) {
+        int hi = b;
+        ++a;
+        while (a < hi) {
+            const int mid = (a + hi) >> 1;
+            if (piv[mid] < v) a = mid + 1; else hi = mid;
+        }
     }
-    int eq = (a < k && piv[a] == v) ? 1 : 0;
-    return 2 * a + eq;
+    return 2 * a + (piv[a] == v ? 1 : 0);
 }
 
 __host__ __device__ __forceinline__ long long cdiv(long long a, long long b) { return (a + b - 1) / b; }

@@ -1,0 +1,24 @@
+"""Sort one C0 workload a few times (for ncu / compute-sanitizer runs)."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_1107_3622_b200 as K  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--n", type=int, default=10_000_000)
+p.add_argument("--kind", default="uniform01")
+p.add_argument("--reps", type=int, default=2)
+a = p.parse_args()
+pristine = K.generate_device(a.n, 20260816, a.kind)
+keys = torch.empty_like(pristine)
+for _ in range(a.reps):
+    keys.copy_(pristine)
+    K.k_sort(keys)
+torch.cuda.synchronize()
+ok = K.is_sorted(keys)
+print("sorted", ok, K.last_stats)
+sys.exit(0 if ok else 1)
