@@ -14,8 +14,9 @@
 //   finishing pass, larger gaps become the next pass's segments.
 //
 // Kernels per pass: seg_prep -> seg_offsets -> pivots -> count -> scan (3) ->
-// scatter -> plan -> finish.  No key crosses to the host; the host reads one
-// small status block per pass to decide whether another pass is needed.
+// scatter -> plan; then local partition rounds (one CTA per segment) and one
+// warp-per-unit finishing launch.  No key crosses to the host; the host reads
+// one small status block per pass to decide whether another pass is needed.
 #include <cfloat>
 #include <cstdio>
 #include <vector>
@@ -30,7 +31,7 @@ constexpr int kScanBlock = 4096;   // count-matrix entries per scan CTA (512 thr
 constexpr int kScanThreads = 512;
 
 // ---------------------------------------------------------------------------
-// finishing-pass work items
+// work lists
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ Item make_item(long long start, long long len, int kind, int src)
 {
@@ -42,55 +43,52 @@ __device__ __forceinline__ Item make_item(long long start, long long len, int ki
     return it;
 }
 
-// single-lane append (init kernels); the plan kernel reserves ranges per CTA
-__device__ __forceinline__ void push_big(DevStatus *st, Item *big, int cap, const Item &it)
+__device__ __forceinline__ Seg make_seg(long long start, long long len, int src)
 {
-    int i = atomicAdd(&st->nbig, 1);
-    if (i >= cap) { st->overflow = 3; return; }
-    big[i] = it;
+    Seg g{};
+    g.start = start;
+    g.len = len;
+    g.src = src;
+    return g;
 }
 
-// ---------------------------------------------------------------------------
-// init / gate
-// ---------------------------------------------------------------------------
-__global__ void k_init_single(long long n, Seg *segs, Item *big, DevStatus *st, int cap)
+// Route one segment at start: > kLocalMax keys -> global pass list,
+// kUnitMax < len <= kLocalMax -> local-partition list, 2..kUnitMax -> unit.
+__device__ __forceinline__ void route_initial(long long a, long long len, Seg *gsegs, Seg *lsegs, Item *units,
+                                              DevStatus *st, int seg_cap, int lseg_cap, int unit_cap)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    if (n > kLeafMax) {
-        Seg g{};
-        g.start = 0;
-        g.len = n;
-        segs[0] = g;
-        st->nseg[0] = 1;
-    } else if (n >= 2) {
-        push_big(st, big, cap, make_item(0, n, kItemBig, 0));
-        st->keys_leaf = (unsigned long long)n;
-        st->leaves = 1;
-        add_bytes(st, kPhGate, 8ull * (unsigned long long)n);    // finiteness gate read
-        add_bytes(st, kPhLeaf, 16ull * (unsigned long long)n);   // on-chip sort read + write
+    if (len > kLocalMax) {
+        int i = atomicAdd(&st->nseg[0], 1);
+        if (i < seg_cap) gsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
+    } else if (len > kLocalBig) {
+        int i = atomicAdd(&st->nlocal_big[0], 1);
+        if (i < lseg_cap) lsegs[lseg_cap - 1 - i] = make_seg(a, len, 0); else st->overflow = 1;
+    } else if (len > kUnitMax) {
+        int i = atomicAdd(&st->nlocal[0], 1);
+        if (i < lseg_cap) lsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
+    } else if (len >= 2) {
+        int i = atomicAdd(&st->nunits, 1);
+        if (i < unit_cap) units[i] = make_item(a, len, kItemUnit, 0); else st->overflow = 1;
+        atomicAdd(&st->keys_leaf, (unsigned long long)len);
+        atomicAdd(&st->leaves, 1ull);
+        add_bytes(st, kPhLeaf, 16ull * (unsigned long long)len);
     }
 }
 
-__global__ void k_init_segmented(const long long *off, long long nseg0, Seg *segs, Item *big, DevStatus *st,
-                                 int seg_cap, int cap)
+__global__ void k_init_single(long long n, Seg *gsegs, Seg *lsegs, Item *units, DevStatus *st, int seg_cap,
+                              int lseg_cap, int unit_cap)
+{
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    route_initial(0, n, gsegs, lsegs, units, st, seg_cap, lseg_cap, unit_cap);
+}
+
+__global__ void k_init_segmented(const long long *off, long long nseg0, Seg *gsegs, Seg *lsegs, Item *units,
+                                 DevStatus *st, int seg_cap, int lseg_cap, int unit_cap)
 {
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nseg0;
          s += (long long)gridDim.x * blockDim.x) {
-        long long a = off[s], b = off[s + 1];
-        long long len = b - a;
-        if (len > kLeafMax) {
-            int i = atomicAdd(&st->nseg[0], 1);
-            if (i >= seg_cap) { st->overflow = 1; continue; }
-            Seg g{};
-            g.start = a;
-            g.len = len;
-            segs[i] = g;
-        } else if (len >= 2) {
-            push_big(st, big, cap, make_item(a, len, kItemBig, 0));
-            atomicAdd(&st->keys_leaf, (unsigned long long)len);
-            atomicAdd(&st->leaves, 1ull);
-            add_bytes(st, kPhLeaf, 16ull * (unsigned long long)len);
-        }
+        const long long a = off[s], b = off[s + 1];
+        route_initial(a, b - a, gsegs, lsegs, units, st, seg_cap, lseg_cap, unit_cap);
     }
 }
 
@@ -109,46 +107,138 @@ __device__ __forceinline__ void gate_flush(long long bad, unsigned pz, unsigned 
     if (nz) atomicOr(&st->neg_zero, 1u);
 }
 
-// Finiteness gate (sort_core.py:50-59) for keys not covered by a level-0
-// count pass: segments of length <= S (they go straight to the finishing pass).
+// Finiteness gate (sort_core.py:50-59) for keys not covered by the level-0
+// count pass: segments of <= kLocalMax keys (they never see a global pass).
 __global__ void k_gate_segments(const double *keys, const long long *off, long long nseg0, long long n_single,
                                 DevStatus *st)
 {
     long long bad = LLONG_MAX;
     unsigned pz = 0, nz = 0;
+    long long checked = 0;
     if (off == nullptr) {
         for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n_single;
-             i += (long long)gridDim.x * blockDim.x)
+             i += (long long)gridDim.x * blockDim.x) {
             gate_one(keys[i], i, bad, pz, nz);
+            ++checked;
+        }
     } else {
-        long long checked = 0;
         for (long long s = blockIdx.x; s < nseg0; s += gridDim.x) {
             long long a = off[s], b = off[s + 1];
-            if (b - a > kLeafMax) continue;  // covered by the level-0 count pass
-            checked += b - a;
-            for (long long i = a + threadIdx.x; i < b; i += blockDim.x) gate_one(keys[i], i, bad, pz, nz);
+            if (b - a > kLocalMax) continue;  // covered by the level-0 count pass
+            for (long long i = a + threadIdx.x; i < b; i += blockDim.x) {
+                gate_one(keys[i], i, bad, pz, nz);
+                ++checked;
+            }
         }
-        if (threadIdx.x == 0) add_bytes(st, kPhGate, 8ull * (unsigned long long)checked);
     }
+    if (checked) add_bytes(st, kPhGate, 8ull * (unsigned long long)checked);
     gate_flush(bad, pz, nz, st);
 }
 
 // ---------------------------------------------------------------------------
-// per-pass segment bookkeeping
+// pivots: the first P keys of a segment are the top of its K-sort tree.
+// Sorted by one warp in registers, de-duplicated (equal keys are one node:
+// the fat pivot), NaN sentinels after them, plus the bucket LUT built by a
+// histogram of pivot buckets and an exclusive scan (a = #pivots in buckets
+// < t, b = #pivots in buckets <= t).
+// ---------------------------------------------------------------------------
+struct PivotScratch {
+    double sp[kPMaxPow2];
+    long long sh[33];
+    int sk;
+};
+
+__device__ void build_pivots(const double *seg, int P, int Treq, double *piv, unsigned *lut, PivotScratch &W,
+                             int &k_out, int &T_out, double &lo_out, double &scale_out)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (wid == 0) {
+        double x[16];
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+            const int i = lane * 16 + r;
+            x[r] = i < P ? seg[i] : CUDART_INF;
+        }
+        warp_bitonic_sort<16>(x);
+#pragma unroll
+        for (int r = 0; r < 16; ++r) W.sp[lane * 16 + r] = x[r];
+    }
+    __syncthreads();
+    long long carry = 0;
+    for (int base = 0; base < P; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const int keep = (i < P && (i == 0 || W.sp[i] != W.sp[i - 1])) ? 1 : 0;
+        long long tot;
+        const long long pos = block_exclusive_scan(keep, W.sh, &tot);
+        if (keep) piv[carry + pos] = W.sp[i];
+        carry += tot;
+    }
+    const int k = (int)carry;
+    if (threadIdx.x < kPivPad) piv[k + threadIdx.x] = CUDART_NAN;
+    __syncthreads();
+    int T = Treq;
+    const double lo = piv[0], hi = piv[k - 1];
+    double scale = 0.0;
+    if (T > 1 && k >= 2 && hi > lo) {
+        scale = (double)T / (hi - lo);
+        if (!(scale > 0.0) || isinf(scale)) T = 1;
+    } else {
+        T = 1;
+    }
+    if (T == 1) scale = 0.0;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) lut[t] = 0u;
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x) atomicAdd(&lut[lut_bucket(piv[j], lo, scale, T)], 1u);
+    __syncthreads();
+    {   // exclusive scan over T buckets, T / blockDim consecutive buckets per thread
+        const int per = (T + blockDim.x - 1) / blockDim.x;
+        const int t0 = threadIdx.x * per;
+        int local = 0;
+        for (int q = 0; q < per; ++q)
+            if (t0 + q < T) local += (int)lut[t0 + q];
+        long long ex = block_exclusive_scan(local, W.sh, nullptr);
+        for (int q = 0; q < per; ++q) {
+            if (t0 + q < T) {
+                const int c = (int)lut[t0 + q];
+                lut[t0 + q] = lut_pack((int)ex, (int)ex + c);
+                ex += c;
+            }
+        }
+    }
+    __syncthreads();
+    k_out = k;
+    T_out = T;
+    lo_out = lo;
+    scale_out = scale;
+}
+
+__host__ __device__ __forceinline__ int pivots_for(long long len)
+{
+    long long P = cdiv(len, kKeysPerPivot);
+    if (P > kPMax) P = kPMax;
+    if (P < 1) P = 1;
+    return (int)P;
+}
+
+__host__ __device__ __forceinline__ int lut_for(int P)
+{
+    int T = P >= 2 ? next_pow2(8 * P) : 1;
+    return T > kLutMax ? kLutMax : T;
+}
+
+// ---------------------------------------------------------------------------
+// global pass bookkeeping
 // ---------------------------------------------------------------------------
 __global__ void k_seg_prep(Seg *segs, const int *nseg)
 {
     int ns = *nseg;
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
         Seg g = segs[s];
-        long long P = cdiv(g.len, kKeysPerPivot);
-        if (P > kPMax) P = kPMax;
-        if (P < 1) P = 1;
-        g.P = (int)P;
+        g.P = pivots_for(g.len);
         g.rows = 2 * g.P + 1;
         g.nch = (int)cdiv(g.len, kChunk);
-        g.T = g.P >= 2 ? next_pow2(4 * g.P) : 1;
-        if (g.T > kLutMax) g.T = kLutMax;
+        g.T = lut_for(g.P);
         segs[s] = g;
     }
 }
@@ -195,75 +285,20 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
     }
 }
 
-// Pivots of each segment: the first P keys (the top of its K-sort tree),
-// sorted and de-duplicated (NaN sentinel after them); plus the bucket LUT
-// and the chunk -> segment map.
 __global__ void __launch_bounds__(256) k_pivots(Seg *segs, const int *nseg, const double *src, double *piv_pool,
-                                                int2 *lut_pool, int *chunk_seg)
+                                                unsigned *lut_pool, int *chunk_seg)
 {
-    __shared__ double sp[kPMaxPow2];
-    __shared__ double cp[kPMax + 1];
-    __shared__ long long sh[33];
-    __shared__ int sk;
-    int ns = *nseg;
+    __shared__ PivotScratch W;
+    __shared__ double piv[kPMax + kPivPad];
+    __shared__ unsigned lut[kLutMax];
+    const int ns = *nseg;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
-        __syncthreads();
-        Seg g = segs[s];
-        const int P = g.P, NP = next_pow2(P);
-        for (int i = threadIdx.x; i < NP; i += blockDim.x) sp[i] = i < P ? src[g.start + i] : CUDART_INF;
-        __syncthreads();
-        for (int kk = 2; kk <= NP; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < NP / 2; i += blockDim.x) {
-                    int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1)), hi = lo + j;
-                    bool asc = (lo & kk) == 0;
-                    double a = sp[lo], b = sp[hi];
-                    if ((a > b) == asc) { sp[lo] = b; sp[hi] = a; }
-                }
-                __syncthreads();
-            }
-        }
-        // de-duplicate (equal keys are one node of the tree: the fat pivot)
-        long long carry = 0;
-        for (int base = 0; base < P; base += blockDim.x) {
-            int i = base + threadIdx.x;
-            int keep = (i < P && (i == 0 || sp[i] != sp[i - 1])) ? 1 : 0;
-            long long tot;
-            long long pos = block_exclusive_scan(keep, sh, &tot);
-            if (keep) cp[carry + pos] = sp[i];
-            carry += tot;
-        }
-        if (threadIdx.x == 0) {
-            sk = (int)carry;
-            cp[carry] = CUDART_NAN;   // sentinel: compares false both ways, even with +/-inf keys
-        }
-        __syncthreads();
-        const int k = sk;
-        for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = cp[i];
-        // LUT over the pivot range (monotone bucket map, ks_internal.cuh)
-        int T = g.T;
-        double lo = cp[0], hi = cp[k - 1], scale = 0.0;
-        if (T > 1 && k >= 2 && hi > lo) {
-            scale = (double)T / (hi - lo);
-            if (!(scale > 0.0) || isinf(scale)) T = 1;
-        } else {
-            T = 1;
-        }
-        if (T == 1) scale = 0.0;
-        for (int t = threadIdx.x; t < T; t += blockDim.x) {
-            // lut[t] = (#{j : bucket(piv_j) < t}, #{j : bucket(piv_j) <= t})
-            int a = 0, b = k;
-            while (a < b) {
-                int mid = (a + b) >> 1;
-                if (lut_bucket(cp[mid], lo, scale, T) < t) a = mid + 1; else b = mid;
-            }
-            int a2 = a, b2 = k;
-            while (a2 < b2) {
-                int mid = (a2 + b2) >> 1;
-                if (lut_bucket(cp[mid], lo, scale, T) <= t) a2 = mid + 1; else b2 = mid;
-            }
-            lut_pool[g.lut_off + t] = make_int2(a, a2);
-        }
+        const Seg g = segs[s];
+        int k, T;
+        double lo, scale;
+        build_pivots(src + g.start, g.P, g.T, piv, lut, W, k, T, lo, scale);
+        for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = piv[i];
+        for (int t = threadIdx.x; t < T; t += blockDim.x) lut_pool[g.lut_off + t] = lut[t];
         for (int c = threadIdx.x; c < g.nch; c += blockDim.x) chunk_seg[g.ch_off + c] = s;
         if (threadIdx.x == 0) {
             segs[s].k = k;
@@ -280,23 +315,24 @@ __global__ void __launch_bounds__(256) k_pivots(Seg *segs, const int *nseg, cons
 // than ballot- or match-based peer aggregation; scripts/mb_hist.cu)
 // ---------------------------------------------------------------------------
 struct PassSmem {
-    double piv[kPMax + 1];
-    int2 lut[kLutMax];
+    double piv[kPMax + kPivPad];
+    unsigned lut[kLutMax];
 };
 
-__device__ __forceinline__ void load_seg(const Seg *segs, int s, const double *piv_pool, const int2 *lut_pool,
+__device__ __forceinline__ void load_seg(const Seg *segs, int s, const double *piv_pool, const unsigned *lut_pool,
                                          Seg &sg, PassSmem &P)
 {
     if (threadIdx.x == 0) sg = segs[s];
     __syncthreads();
-    for (int i = threadIdx.x; i <= sg.k; i += blockDim.x) P.piv[i] = piv_pool[sg.piv_off + i];
+    for (int i = threadIdx.x; i < sg.k + kPivPad; i += blockDim.x)
+        P.piv[i] = i < sg.k ? piv_pool[sg.piv_off + i] : CUDART_NAN;
     for (int i = threadIdx.x; i < sg.T; i += blockDim.x) P.lut[i] = lut_pool[sg.lut_off + i];
 }
 
 template <bool kGate>
 __global__ void __launch_bounds__(kCountThreads) k_count(const Seg *segs, const int *chunk_seg, const DevStatus *cst,
                                                          const double *src, const double *piv_pool,
-                                                         const int2 *lut_pool, unsigned *mat, DevStatus *st)
+                                                         const unsigned *lut_pool, unsigned *mat, DevStatus *st)
 {
     constexpr int U = 8;   // keys in flight per lane
     __shared__ PassSmem P;
@@ -320,22 +356,22 @@ __global__ void __launch_bounds__(kCountThreads) k_count(const Seg *segs, const 
         const int cnt = (int)min((long long)kChunk, sg.len - (long long)j * kChunk);
         const int T = sg.T;
         const double lo = sg.lo, scale = sg.scale;
-        const double *in = src + base;
-        for (int i0 = 0; i0 < cnt; i0 += U * kCountThreads) {
+        const double *in = src + base + threadIdx.x;
+        int i0 = 0;
+        for (; i0 + U * kCountThreads <= cnt; i0 += U * kCountThreads) {   // full blocks: no bounds checks
             double v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * kCountThreads + threadIdx.x;
-                v[u] = i < cnt ? in[i] : 0.0;
-            }
+            for (int u = 0; u < U; ++u) v[u] = in[i0 + u * kCountThreads];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int i = i0 + u * kCountThreads + threadIdx.x;
-                if (i < cnt) {
-                    if (kGate) gate_one(v[u], base + i, bad, pz, nz);
-                    atomicAdd(&hist[classify(v[u], P.piv, P.lut, lo, scale, T)], 1u);
-                }
+                if (kGate) gate_one(v[u], base + threadIdx.x + i0 + u * kCountThreads, bad, pz, nz);
+                atomicAdd(&hist[classify(v[u], P.piv, P.lut, lo, scale, T)], 1u);
             }
+        }
+        for (int i = i0 + threadIdx.x; i < cnt; i += kCountThreads) {
+            const double v = src[base + i];
+            if (kGate) gate_one(v, base + i, bad, pz, nz);
+            atomicAdd(&hist[classify(v, P.piv, P.lut, lo, scale, T)], 1u);
         }
         __syncthreads();
         for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) mat[sg.mat_off + (long long)c * sg.nch + j] = hist[c];
@@ -418,23 +454,23 @@ __device__ __forceinline__ long long class_start(const Seg &g, const long long *
 // ---------------------------------------------------------------------------
 struct ScatterSmem {
     double stage[kTile];
-    long long cur[kRowsMax];
+    long long sdst[kTile];     // destination of each staged key (-1: equality run that is filled later)
+    long long cur[kRowsMax];   // class cursors; LLONG_MIN marks classes that are not written
     PassSmem P;
     unsigned hist[kRowsMax + 1];
     unsigned off[kRowsMax + 1];
-    unsigned short cls[kTile];
-    unsigned char skip[kRowsMax + 1];
     long long sh[33];
     Seg sg;
 };
 
-__global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const int *chunk_seg, const DevStatus *cst,
-                                                          const double *src, double *dst, const double *piv_pool,
-                                                          const int2 *lut_pool, const long long *moff)
+__global__ void __launch_bounds__(kPassThreads, 2) k_scatter(const Seg *segs, const int *chunk_seg,
+                                                             const DevStatus *cst, const double *src, double *dst,
+                                                             const double *piv_pool, const unsigned *lut_pool,
+                                                             const long long *moff)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
-    constexpr int E = kTile / kPassThreads;   // keys per thread per tile (16)
+    constexpr int E = kTile / kPassThreads;   // keys per thread per tile (8)
     int cached = -1;
     const int nchunks = cst->nchunks;
     for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
@@ -452,9 +488,10 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
         const int rows = g.rows, nch = g.nch, T = g.T;
         const double lo = g.lo, scale = g.scale;
         for (int c = threadIdx.x; c < rows; c += blockDim.x) {
-            S.cur[c] = g.start + (moff[g.mat_off + (long long)c * nch + j] - base_i);
-            const long long tot = class_start(g, moff, base_i, c + 1) - class_start(g, moff, base_i, c);
-            S.skip[c] = ((c & 1) && tot >= kFillMin) ? 1 : 0;
+            const long long c0 = class_start(g, moff, base_i, c);
+            const long long tot = class_start(g, moff, base_i, c + 1) - c0;
+            const bool skip = (c & 1) && tot >= kFillMin;   // long equality run: filled by the finish pass
+            S.cur[c] = skip ? LLONG_MIN : g.start + (moff[g.mat_off + (long long)c * nch + j] - base_i);
         }
         const double *in = src + base;
         for (int t0 = 0; t0 < cnt; t0 += kTile) {
@@ -463,17 +500,23 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
             __syncthreads();
             double v[E];
             unsigned cl[E], rk[E];
+            if (tcnt == kTile) {
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int i = e * kPassThreads + threadIdx.x;
-                v[e] = i < tcnt ? in[t0 + i] : 0.0;
-            }
+                for (int e = 0; e < E; ++e) v[e] = in[t0 + e * kPassThreads + threadIdx.x];
 #pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int i = e * kPassThreads + threadIdx.x;
-                if (i < tcnt) {
+                for (int e = 0; e < E; ++e) {
                     cl[e] = (unsigned)classify(v[e], S.P.piv, S.P.lut, lo, scale, T);
                     rk[e] = atomicAdd(&S.hist[cl[e]], 1u);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const int i = e * kPassThreads + threadIdx.x;
+                    v[e] = i < tcnt ? in[t0 + i] : 0.0;
+                    if (i < tcnt) {
+                        cl[e] = (unsigned)classify(v[e], S.P.piv, S.P.lut, lo, scale, T);
+                        rk[e] = atomicAdd(&S.hist[cl[e]], 1u);
+                    }
                 }
             }
             __syncthreads();
@@ -491,39 +534,146 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
                 const int i = e * kPassThreads + threadIdx.x;
                 if (i < tcnt) {
                     const unsigned p = S.off[cl[e]] + rk[e];
+                    const long long cb = S.cur[cl[e]];
                     S.stage[p] = v[e];
-                    S.cls[p] = (unsigned short)cl[e];
+                    S.sdst[p] = cb < 0 ? -1 : cb + rk[e];
                 }
             }
             __syncthreads();
-            for (int p = threadIdx.x; p < tcnt; p += blockDim.x) {
-                const int c = S.cls[p];
-                if (!S.skip[c]) dst[S.cur[c] + (p - (long long)S.off[c])] = S.stage[p];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const int p = e * kPassThreads + threadIdx.x;
+                if (p < tcnt) {
+                    const long long d = S.sdst[p];
+                    if (d >= 0) dst[d] = S.stage[p];
+                }
             }
             __syncthreads();
-            for (int c = threadIdx.x; c < rows; c += blockDim.x) S.cur[c] += S.hist[c];
+            for (int c = threadIdx.x; c < rows; c += blockDim.x)
+                if (S.cur[c] >= 0) S.cur[c] += S.hist[c];
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// plan: turn class extents into next-pass segments and finishing work.
-// Each thread owns one pivot j (<= 512 per segment): the gap below it (class
-// 2j) and its equality run (class 2j+1).  A gap of <= kUnitMax keys plus its
-// short equality run is one warp unit; longer equality runs are fills; gaps
-// of kUnitMax+1..S keys are CTA "big" items; larger gaps become segments of
-// the next pass.  Items are reserved per CTA with one atomic per list.
+// emission of finishing work (shared by the global plan and the local
+// partitioner).  Each thread owns one pivot j: the gap below it (class 2j,
+// gl keys at ag) and its equality run (class 2j+1, el keys at ae).
+//  * gap <= kUnitMax (+ its short equality run)  -> one warp unit
+//  * kUnitMax < gap <= kLocalMax                 -> local-partition segment
+//  * gap > kLocalMax                             -> next global pass
+//  * equality run >= kFillMin                    -> fill (never scattered)
+// Lists are reserved per CTA with one atomic each.
+// ---------------------------------------------------------------------------
+struct EmitOut {
+    long long unit_keys, fill_keys, items;
+};
+
+struct EmitArgs {
+    Seg *gnext;
+    int *ngnext;
+    int gcap;
+    Seg *lnext;
+    int *nlnext;       // small local segments, stored from index 0 upwards
+    int *nlnext_big;   // big local segments (> kLocalBig), stored from index lcap-1 downwards
+    int lcap;
+    Item *units;
+    int ucap;
+};
+
+__device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
+                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase)
+{
+    const bool eq_written = el > 0 && el < kFillMin;   // the scatter wrote these keys
+    int u_gap = 0, l_gap = 0, lb_gap = 0, g_gap = 0, u_eq = 0, f_eq = 0;
+    long long ulen_gap = gl;
+    if (have && (gl >= 2 || (gl == 1 && dst_id == 1))) {
+        if (gl <= kUnitMax) {
+            u_gap = 1;
+            if (eq_written && gl + el <= kUnitMax) ulen_gap += el;
+        } else if (gl <= kLocalBig) {
+            l_gap = 1;
+        } else if (gl <= kLocalMax) {
+            lb_gap = 1;
+        } else {
+            g_gap = 1;
+        }
+    }
+    const bool eq_packed = u_gap && ulen_gap > gl;
+    if (have && el >= kFillMin) f_eq = 1;
+    else if (have && eq_written && !eq_packed && dst_id == 1) u_eq = 1;
+    const int nu = u_gap + u_eq + f_eq;
+    long long tu, tl, tlb, tg;
+    const long long xu = block_exclusive_scan(nu, sh, &tu);
+    const long long xl = block_exclusive_scan(l_gap, sh, &tl);
+    const long long xlb = block_exclusive_scan(lb_gap, sh, &tlb);
+    const long long xg = block_exclusive_scan(g_gap, sh, &tg);
+    if (threadIdx.x == 0) {
+        sbase[0] = tu ? atomicAdd(&st->nunits, (int)tu) : 0;
+        sbase[1] = tl ? atomicAdd(A.nlnext, (int)tl) : 0;
+        sbase[2] = tg ? atomicAdd(A.ngnext, (int)tg) : 0;
+        sbase[3] = tlb ? atomicAdd(A.nlnext_big, (int)tlb) : 0;
+    }
+    __syncthreads();
+    long long ui = sbase[0] + xu;
+    if (u_gap) {
+        if (ui < A.ucap) A.units[ui] = make_item(ag, ulen_gap, kItemUnit, dst_id); else st->overflow = 3;
+        ++ui;
+    }
+    if (u_eq) {
+        if (ui < A.ucap) A.units[ui] = make_item(ae, el, kItemUnit, dst_id); else st->overflow = 3;
+        ++ui;
+    }
+    if (f_eq) {
+        Item it = make_item(ae, el, kItemFill, dst_id);
+        it.value = pv;
+        if (ui < A.ucap) A.units[ui] = it; else st->overflow = 3;
+    }
+    if (l_gap) {
+        const long long li = sbase[1] + xl;
+        if (li < A.lcap) A.lnext[li] = make_seg(ag, gl, dst_id); else st->overflow = 4;
+    }
+    if (lb_gap) {
+        const long long li = A.lcap - 1 - (sbase[3] + xlb);
+        if (li >= 0) A.lnext[li] = make_seg(ag, gl, dst_id); else st->overflow = 4;
+    }
+    if (g_gap) {
+        const long long gi = sbase[2] + xg;
+        if (gi < A.gcap) A.gnext[gi] = make_seg(ag, gl, dst_id); else st->overflow = 4;
+    }
+    long long t_fk, t_uk;
+    block_exclusive_scan(f_eq ? el : 0, sh, &t_fk);
+    block_exclusive_scan((u_gap ? ulen_gap : 0) + (u_eq ? el : 0), sh, &t_uk);
+    EmitOut o;
+    o.unit_keys = t_uk;
+    o.fill_keys = t_fk;
+    o.items = tu;
+    return o;
+}
+
+__device__ __forceinline__ void account_partition(DevStatus *st, long long len, const EmitOut &o)
+{
+    // algorithmic bytes: count reads 8B/key; scatter reads 8B/key and writes 8B
+    // per key it places; units read+write 16B/key; fills write 8B/key
+    add_bytes(st, kPhCount, 8ull * len);
+    add_bytes(st, kPhScatter, 8ull * len + 8ull * (len - o.fill_keys));
+    add_bytes(st, kPhLeaf, 16ull * o.unit_keys + 8ull * o.fill_keys);
+    atomicAdd(&st->keys_partitioned, (unsigned long long)len);
+    atomicAdd(&st->keys_leaf, (unsigned long long)o.unit_keys);
+    atomicAdd(&st->leaves, (unsigned long long)o.items);
+}
+
+// ---------------------------------------------------------------------------
+// plan (global pass): class extents from the scanned count matrix
 // ---------------------------------------------------------------------------
 constexpr int kPlanThreads = 512;
+static_assert(kPMax + 1 <= kPlanThreads, "one pivot pair per thread");
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const int *nseg, const double *piv_pool,
-                                                       const long long *moff, Seg *next, int *nnext, Item *units,
-                                                       Item *big, DevStatus *st, int dst_id, int seg_cap,
-                                                       int unit_cap, int big_cap)
+                                                       const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
 {
     __shared__ long long sh[33];
-    __shared__ long long sbase[3];
-    static_assert(kPMax + 1 <= kPlanThreads, "one pivot pair per thread");
+    __shared__ long long sbase[4];
     const int ns = *nseg;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
         __syncthreads();
@@ -532,90 +682,119 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
         const int j = threadIdx.x;
         const bool have = j <= g.k;
         long long ag = 0, gl = 0, ae = 0, el = 0;
+        double pv = 0.0;
         if (have) {
             ag = class_start(g, moff, base_i, 2 * j);
             ae = class_start(g, moff, base_i, 2 * j + 1);
             gl = ae - ag;
-            if (j < g.k) el = class_start(g, moff, base_i, 2 * j + 2) - ae;
-        }
-        const bool eq_written = el > 0 && el < kFillMin;   // the scatter wrote these keys
-        // decide this pair's items
-        int u_gap = 0, b_gap = 0, n_gap = 0, u_eq = 0, f_eq = 0;
-        long long ulen_gap = gl;
-        if (gl >= 2 || (gl == 1 && dst_id == 1)) {
-            if (gl <= kUnitMax) {
-                u_gap = 1;
-                if (eq_written && gl + el <= kUnitMax) ulen_gap += el;
-            } else if (gl <= kLeafMax) {
-                b_gap = 1;
-            } else {
-                n_gap = 1;
+            if (j < g.k) {
+                el = class_start(g, moff, base_i, 2 * j + 2) - ae;
+                pv = piv_pool[g.piv_off + j];
             }
         }
-        const bool eq_packed = u_gap && ulen_gap > gl;
-        if (el >= kFillMin) f_eq = 1;
-        else if (eq_written && !eq_packed && dst_id == 1) u_eq = 1;
-        const int nu = u_gap + u_eq + f_eq;
-        long long tu, tb, tn;
-        const long long xu = block_exclusive_scan(nu, sh, &tu);
-        const long long xb = block_exclusive_scan(b_gap, sh, &tb);
-        const long long xn = block_exclusive_scan(n_gap, sh, &tn);
-        if (threadIdx.x == 0) {
-            sbase[0] = tu ? atomicAdd(&st->nunits, (int)tu) : 0;
-            sbase[1] = tb ? atomicAdd(&st->nbig, (int)tb) : 0;
-            sbase[2] = tn ? atomicAdd(nnext, (int)tn) : 0;
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase);
+        if (threadIdx.x == 0) account_partition(st, g.len, o);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// local partition: one CTA takes one segment (<= kLocalMax keys, L2-resident)
+// and performs the same K-sort multi-level partition without any grid-wide
+// step: pivots, shared-memory class histogram, scan, scatter into the other
+// buffer, emission of units / next-round segments.  CTAs pull segments from
+// a device work counter.
+// ---------------------------------------------------------------------------
+struct LocalSmem {
+    PivotScratch W;
+    double piv[kPMax + kPivPad];
+    unsigned lut[kLutMax];
+    unsigned hist[kRowsMax + 1];
+    unsigned cursor[kRowsMax + 1];
+    long long sh[33];
+    long long sbase[4];
+    int item;
+};
+
+__global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const int *nlocal, const int *nlocal_big,
+                                                         int lcap, EmitArgs A, DevStatus *st, double *keys,
+                                                         double *tmp)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LocalSmem &L = *reinterpret_cast<LocalSmem *>(smem_raw);
+    const int nb = *nlocal_big, n = *nlocal + nb;
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) L.item = atomicAdd(&st->local_next, 1);
+        __syncthreads();
+        const int d = L.item;
+        if (d >= n) break;
+        // big segments first (longest-processing-time order), from the top of the list
+        const Seg g = d < nb ? lsegs[lcap - 1 - d] : lsegs[d - nb];
+        const double *src = (g.src ? tmp : keys) + g.start;
+        double *dst = (g.src ? keys : tmp) + g.start;
+        const int dst_id = g.src ? 0 : 1;
+        const int m = (int)g.len;
+        const int P = pivots_for(m);
+        int k, T;
+        double lo, scale;
+        build_pivots(src, P, lut_for(P), L.piv, L.lut, L.W, k, T, lo, scale);
+        const int rows = 2 * k + 1;
+        for (int c = threadIdx.x; c < rows; c += blockDim.x) L.hist[c] = 0;
+        __syncthreads();
+        constexpr int U = 8;
+        int i0 = 0;
+        for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = src[i0 + u * kLocalThreads + threadIdx.x];
+#pragma unroll
+            for (int u = 0; u < U; ++u) atomicAdd(&L.hist[classify(v[u], L.piv, L.lut, lo, scale, T)], 1u);
+        }
+        for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads)
+            atomicAdd(&L.hist[classify(src[i], L.piv, L.lut, lo, scale, T)], 1u);
+        __syncthreads();
+        {   // exclusive scan of the class histogram -> class starts (2 classes per thread)
+            const int c0 = 2 * threadIdx.x;
+            const unsigned h0 = c0 < rows ? L.hist[c0] : 0u;
+            const unsigned h1 = c0 + 1 < rows ? L.hist[c0 + 1] : 0u;
+            const long long ex = block_exclusive_scan((long long)h0 + h1, L.sh, nullptr);
+            if (c0 < rows) L.cursor[c0] = (unsigned)ex;
+            if (c0 + 1 < rows) L.cursor[c0 + 1] = (unsigned)ex + h0;
         }
         __syncthreads();
-        long long ui = sbase[0] + xu;
-        if (u_gap) {
-            if (ui < unit_cap) units[ui] = make_item(g.start + ag, ulen_gap, kItemUnit, dst_id);
-            else st->overflow = 3;
-            ++ui;
-        }
-        if (u_eq) {
-            if (ui < unit_cap) units[ui] = make_item(g.start + ae, el, kItemUnit, dst_id);
-            else st->overflow = 3;
-            ++ui;
-        }
-        if (f_eq) {
-            Item it = make_item(g.start + ae, el, kItemFill, dst_id);
-            it.value = piv_pool[g.piv_off + j];
-            if (ui < unit_cap) units[ui] = it;
-            else st->overflow = 3;
-        }
-        if (b_gap) {
-            const long long bi = sbase[1] + xb;
-            if (bi < big_cap) big[bi] = make_item(g.start + ag, gl, kItemBig, dst_id);
-            else st->overflow = 5;
-        }
-        if (n_gap) {
-            const long long ni = sbase[2] + xn;
-            if (ni < seg_cap) {
-                Seg n2{};
-                n2.start = g.start + ag;
-                n2.len = gl;
-                next[ni] = n2;
-            } else {
-                st->overflow = 4;
+        i0 = 0;
+        for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = src[i0 + u * kLocalThreads + threadIdx.x];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = classify(v[u], L.piv, L.lut, lo, scale, T);
+                if (!(c & 1) || L.hist[c] < (unsigned)kFillMin) dst[atomicAdd(&L.cursor[c], 1u)] = v[u];
             }
         }
-        // algorithmic bytes (count reads 8B/key; scatter reads 8B/key and writes 8B
-        // per key it places; units/big read+write 16B/key; fills write 8B/key)
-        const long long fk = f_eq ? el : 0;
-        const long long uk = (u_gap ? ulen_gap : 0) + (u_eq ? el : 0);
-        const long long bk = b_gap ? gl : 0;
-        long long t_fk, t_uk, t_bk;
-        block_exclusive_scan(fk, sh, &t_fk);
-        block_exclusive_scan(uk, sh, &t_uk);
-        block_exclusive_scan(bk, sh, &t_bk);
-        if (threadIdx.x == 0) {
-            add_bytes(st, kPhCount, 8ull * g.len);
-            add_bytes(st, kPhScatter, 8ull * g.len + 8ull * (g.len - t_fk));
-            add_bytes(st, kPhLeaf, 16ull * (t_uk + t_bk) + 8ull * t_fk);
-            atomicAdd(&st->keys_partitioned, (unsigned long long)g.len);
-            atomicAdd(&st->keys_leaf, (unsigned long long)(t_uk + t_bk));
-            atomicAdd(&st->leaves, (unsigned long long)(tu + tb));
+        for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads) {
+            const double v = src[i];
+            const int c = classify(v, L.piv, L.lut, lo, scale, T);
+            if (!(c & 1) || L.hist[c] < (unsigned)kFillMin) dst[atomicAdd(&L.cursor[c], 1u)] = v;
         }
+        __syncthreads();
+        // class starts = cursor - (keys written); emit per pivot pair
+        const int j = threadIdx.x;
+        const bool have = j <= k;
+        long long ag = 0, gl = 0, ae = 0, el = 0;
+        double pv = 0.0;
+        if (have) {
+            gl = L.hist[2 * j];
+            ag = (long long)L.cursor[2 * j] - gl;
+            if (j < k) {
+                el = L.hist[2 * j + 1];
+                ae = (long long)L.cursor[2 * j + 1] - (el < kFillMin ? el : 0);
+                pv = L.piv[j];
+            }
+        }
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase);
+        if (threadIdx.x == 0) account_partition(st, g.len, o);
     }
 }
 
@@ -696,126 +875,8 @@ __global__ void __launch_bounds__(kUnitWarps * 32, 3) k_finish_units(const Item 
 }
 
 // ---------------------------------------------------------------------------
-// finish (big): one CTA per gap of kUnitMax+1 .. S keys: 16 warps sort runs of
-// N/16 keys in registers, then four merge-path passes in shared memory.
+// host plumbing
 // ---------------------------------------------------------------------------
-struct BigSmem {
-    double s[sidx_size(kLeafMax)];
-};
-
-template <int E>
-__device__ __forceinline__ void warp_sort_smem(double *s, int off, int m)
-{
-    // sort s[off .. off+m) (sidx layout) in place with one warp, m <= 32*E
-    const int lane = threadIdx.x & 31;
-    double x[E];
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const int i = lane * E + r;
-        x[r] = i < m ? s[sidx(off + i)] : CUDART_INF;
-    }
-    warp_bitonic_sort<E>(x);
-#pragma unroll
-    for (int r = 0; r < E; ++r) {
-        const int i = lane * E + r;
-        if (i < m) s[sidx(off + i)] = x[r];
-    }
-}
-
-// block sort of s[0..N) (N = 512*E, padded with +inf): 16 warps x (32E-key runs), then merge passes
-template <int E>
-__device__ __forceinline__ void block_sort_smem(double *s)
-{
-    constexpr int N = 512 * E;
-    const int wid = threadIdx.x >> 5;
-    warp_sort_smem<E>(s, wid * 32 * E, 32 * E);
-    __syncthreads();
-#pragma unroll 1
-    for (int size = 32 * E; size < N; size <<= 1) {
-        const int o = threadIdx.x * E;
-        const int g0 = o & ~(2 * size - 1);
-        const int dg = o - g0;
-        const int a = merge_path(s, g0, g0 + size, size, dg);
-        double y[E];
-        merge_serial<E>(s, g0, g0 + size, size, a, dg - a, y);
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < E; ++r) s[sidx(o + r)] = y[r];
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kBigThreads) k_finish_big(const Item *big, const DevStatus *cst, double *keys,
-                                                            const double *tmp)
-{
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    BigSmem &F = *reinterpret_cast<BigSmem *>(smem_raw);
-    if (abort_requested(cst)) return;
-    const int n = cst->nbig;
-    for (int d = blockIdx.x; d < n; d += gridDim.x) {
-        const Item it = big[d];
-        const double *in = (it.src ? tmp : keys) + it.start;
-        double *out = keys + it.start;
-        const int m = it.len;
-        __syncthreads();
-        if (m <= kUnitMax) {   // initial small segments
-            const int lane = threadIdx.x & 31;
-            if (threadIdx.x < 32) {
-                if (m <= 32) warp_unit_sort<1>(in, out, m, F.s);
-                else if (m <= 64) warp_unit_sort<2>(in, out, m, F.s);
-                else if (m <= 128) warp_unit_sort<4>(in, out, m, F.s);
-                else if (m <= 256) warp_unit_sort<8>(in, out, m, F.s);
-                else warp_unit_sort<16>(in, out, m, F.s);
-            }
-            (void)lane;
-            continue;
-        }
-        const int N = next_pow2(m);
-        for (int i = threadIdx.x; i < N; i += blockDim.x) F.s[sidx(i)] = i < m ? in[i] : CUDART_INF;
-        __syncthreads();
-        if (N <= 1024) block_sort_smem<2>(F.s);
-        else if (N <= 2048) block_sort_smem<4>(F.s);
-        else if (N <= 4096) block_sort_smem<8>(F.s);
-        else block_sort_smem<16>(F.s);
-        for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = F.s[sidx(i)];
-    }
-}
-
-// ---------------------------------------------------------------------------
-// host side
-// ---------------------------------------------------------------------------
-static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
-
-FastLayout fast_layout(long long n, long long nseg0)
-{
-    FastLayout L{};
-    L.n = n;
-    L.seg_cap = (int)(n / (kLeafMax + 1) + 2);
-    const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i  (P_i <= ceil(len/64))
-    L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
-    L.lut_cap = (int)(8 * psum + kLutMax);                       // sum of T_i (T_i < 8 P_i)
-    L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
-    L.mat_cap = (2 * psum + L.seg_cap) + (long long)(2 * kPMax + 1) * (2 * (n / kChunk) + 2);
-    L.unit_cap = (int)(2 * psum + 2 * L.seg_cap + 2);            // <= 2 items per pivot pair
-    L.big_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);
-    L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
-    size_t off = 0;
-    L.o_status = off; off = align_up(off + sizeof(DevStatus));
-    L.o_seg[0] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
-    L.o_seg[1] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
-    L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
-    L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
-    L.o_lut = off; off = align_up(off + sizeof(int2) * L.lut_cap);
-    L.o_mat = off; off = align_up(off + sizeof(unsigned) * L.mat_cap);
-    L.o_moff = off; off = align_up(off + sizeof(long long) * L.mat_cap);
-    L.o_bsum = off; off = align_up(off + sizeof(long long) * L.bsum_cap);
-    L.o_units = off; off = align_up(off + sizeof(Item) * L.unit_cap);
-    L.o_big = off; off = align_up(off + sizeof(Item) * L.big_cap);
-    L.o_tmp = off; off = align_up(off + sizeof(double) * (size_t)n);
-    L.total = off;
-    return L;
-}
-
 static int sm_count()
 {
     int dev = 0, sms = 148;
@@ -887,6 +948,44 @@ class Launcher {
     int total_ = 0;
 };
 
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+FastLayout fast_layout(long long n, long long nseg0)
+{
+    FastLayout L{};
+    L.n = n;
+    L.seg_cap = (int)(n / (kLocalMax + 1) + 2);                  // global-pass segments
+    L.lseg_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);          // local-partition segments per round
+    const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
+    L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
+    L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
+    L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
+    L.mat_cap = (2 * psum + L.seg_cap) + (long long)(2 * kPMax + 1) * (2 * (n / kChunk) + 2);
+    // finishing items emitted by one round <= 2 per pivot + 1 per segment; the list is
+    // flushed whenever it is more than half full, so twice that bound suffices
+    L.unit_cap = (int)(2 * (2 * (n / kKeysPerPivot) + 3 * (long long)L.lseg_cap + 2 * L.seg_cap) + 4096);
+    L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
+    size_t off = 0;
+    L.o_status = off; off = align_up(off + sizeof(DevStatus));
+    L.o_seg[0] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
+    L.o_seg[1] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
+    L.o_lseg[0] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
+    L.o_lseg[1] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
+    L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
+    L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
+    L.o_lut = off; off = align_up(off + sizeof(unsigned) * L.lut_cap);
+    L.o_mat = off; off = align_up(off + sizeof(unsigned) * L.mat_cap);
+    L.o_moff = off; off = align_up(off + sizeof(long long) * L.mat_cap);
+    L.o_bsum = off; off = align_up(off + sizeof(long long) * L.bsum_cap);
+    L.o_units = off; off = align_up(off + sizeof(Item) * L.unit_cap);
+    L.o_tmp = off; off = align_up(off + sizeof(double) * (size_t)n);
+    L.total = off;
+    return L;
+}
+
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
               cudaStream_t stream, bool profile, FastResult *res)
 {
@@ -895,60 +994,74 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     char *w = static_cast<char *>(ws);
     DevStatus *st = reinterpret_cast<DevStatus *>(w + L.o_status);
     Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.o_seg[0]), reinterpret_cast<Seg *>(w + L.o_seg[1])};
+    Seg *lsegs[2] = {reinterpret_cast<Seg *>(w + L.o_lseg[0]), reinterpret_cast<Seg *>(w + L.o_lseg[1])};
     int *chunk_seg = reinterpret_cast<int *>(w + L.o_chunk);
     double *piv = reinterpret_cast<double *>(w + L.o_piv);
-    int2 *lut = reinterpret_cast<int2 *>(w + L.o_lut);
+    unsigned *lut = reinterpret_cast<unsigned *>(w + L.o_lut);
     unsigned *mat = reinterpret_cast<unsigned *>(w + L.o_mat);
     long long *moff = reinterpret_cast<long long *>(w + L.o_moff);
     long long *bsum = reinterpret_cast<long long *>(w + L.o_bsum);
     Item *units = reinterpret_cast<Item *>(w + L.o_units);
-    Item *big = reinterpret_cast<Item *>(w + L.o_big);
     double *tmp = reinterpret_cast<double *>(w + L.o_tmp);
 
     KS_CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem)));
-    KS_CK(cudaFuncSetAttribute(k_finish_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(BigSmem)));
+    KS_CK(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LocalSmem)));
     const int sms = sm_count();
-    int occ_count = 1, occ_scatter = 1, occ_units = 1, occ_big = 1;
+    int occ_count = 1, occ_scatter = 1, occ_units = 1, occ_local = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_count, k_count<false>, kCountThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_scatter, k_scatter, kPassThreads, sizeof(ScatterSmem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_units, k_finish_units, kUnitWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_big, k_finish_big, kBigThreads, sizeof(BigSmem));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_local, k_local, kLocalThreads, sizeof(LocalSmem));
     const int g_count = sms * (occ_count > 0 ? occ_count : 1);
     const int g_scatter = sms * (occ_scatter > 0 ? occ_scatter : 1);
     const int g_units = sms * (occ_units > 0 ? occ_units : 1);
-    const int g_big = sms * (occ_big > 0 ? occ_big : 1);
+    const int g_local = sms * (occ_local > 0 ? occ_local : 1);
     const int g_scan = sms * 2;
     const int g_seg = sms * 4;
     Launcher K(stream, profile);
 
     DevStatus h{};
+    auto sync_status = [&]() -> int {
+        KS_CK(cudaGetLastError());
+        KS_CK(cudaMemcpyAsync(&h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+        KS_CK(cudaStreamSynchronize(stream));
+        return h.overflow ? KS_CUDA_ERROR : KS_OK;
+    };
+    auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
+    auto flush_units = [&]() {
+        K.run(kPhLeaf, [&] { k_finish_units<<<g_units, kUnitWarps * 32, 0, stream>>>(units, st, keys, tmp); });
+        cudaMemsetAsync(&st->nunits, 0, sizeof(int), stream);
+    };
+
     KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
     KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
-
     if (d_off == nullptr) {
-        K.run(kPhGate, [&] { k_init_single<<<1, 32, 0, stream>>>(n, segs[0], big, st, L.big_cap); });
-        if (n <= kLeafMax)
-            K.run(kPhGate, [&] { k_gate_segments<<<sms, 256, 0, stream>>>(keys, nullptr, 0, n, st); });
+        K.run(kPhGate, [&] {
+            k_init_single<<<1, 32, 0, stream>>>(n, segs[0], lsegs[0], units, st, L.seg_cap, L.lseg_cap, L.unit_cap);
+        });
+        if (n <= kLocalMax)
+            K.run(kPhGate, [&] { k_gate_segments<<<sms * 2, 256, 0, stream>>>(keys, nullptr, 0, n, st); });
     } else {
         K.run(kPhGate, [&] {
-            k_init_segmented<<<sms, 256, 0, stream>>>(d_off, nseg0, segs[0], big, st, L.seg_cap, L.big_cap);
+            k_init_segmented<<<sms, 256, 0, stream>>>(d_off, nseg0, segs[0], lsegs[0], units, st, L.seg_cap,
+                                                      L.lseg_cap, L.unit_cap);
         });
         K.run(kPhGate, [&] { k_gate_segments<<<sms * 4, 256, 0, stream>>>(keys, d_off, nseg0, 0, st); });
     }
-    KS_CK(cudaGetLastError());
-    KS_CK(cudaMemcpyAsync(&h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
-    KS_CK(cudaStreamSynchronize(stream));
-    if (h.overflow) return KS_CUDA_ERROR;
+    int rc = sync_status();
+    if (rc != KS_OK) return rc;
 
+    // global passes (segments > kLocalMax)
     int level = 0;
     int cur = 0;
-    bool finished_once = false;
-    while (h.nseg[cur] > 0) {
+    while (h.nseg[cur] > 0 && !aborted()) {
         const double *src = (level & 1) ? tmp : keys;
         double *dst = (level & 1) ? keys : tmp;
         const int dst_id = (level & 1) ? 0 : 1;
         int *nseg_cur = &st->nseg[cur];
         int *nseg_next = &st->nseg[cur ^ 1];
+        EmitArgs A{segs[cur ^ 1], nseg_next, L.seg_cap, lsegs[0], &st->nlocal[0], &st->nlocal_big[0], L.lseg_cap, units,
+                   L.unit_cap};
         K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[cur], nseg_cur); });
         K.run(kPhPivots, [&] {
             k_seg_offsets<<<1, 1024, 0, stream>>>(segs[cur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
@@ -970,33 +1083,46 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                                                                                lut, moff);
         });
         KS_CK(cudaMemsetAsync(nseg_next, 0, sizeof(int), stream));
-        K.run(kPhPlan, [&] {
-            k_plan<<<g_seg, kPlanThreads, 0, stream>>>(segs[cur], nseg_cur, piv, moff, segs[cur ^ 1], nseg_next, units,
-                                                       big, st, dst_id, L.seg_cap, L.unit_cap, L.big_cap);
-        });
-        K.run(kPhLeaf, [&] { k_finish_units<<<g_units, kUnitWarps * 32, 0, stream>>>(units, st, keys, tmp); });
-        K.run(kPhLeaf, [&] {
-            k_finish_big<<<g_big, kBigThreads, sizeof(BigSmem), stream>>>(big, st, keys, tmp);
-        });
-        finished_once = true;
-        KS_CK(cudaMemsetAsync(&st->nunits, 0, 2 * sizeof(int), stream));   // nunits, nbig
-        KS_CK(cudaGetLastError());
-        KS_CK(cudaMemcpyAsync(&h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
-        KS_CK(cudaStreamSynchronize(stream));
+        K.run(kPhPlan, [&] { k_plan<<<g_seg, kPlanThreads, 0, stream>>>(segs[cur], nseg_cur, piv, moff, A, st, dst_id); });
+        rc = sync_status();
+        if (rc != KS_OK) return rc;
         ++level;
         cur ^= 1;
-        if (h.overflow) return KS_CUDA_ERROR;
-        if (h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero)) break;
+        if (!aborted() && h.nunits > L.unit_cap / 2) flush_units();
     }
-    if (!finished_once) {
-        K.run(kPhLeaf, [&] {
-            k_finish_big<<<g_big, kBigThreads, sizeof(BigSmem), stream>>>(big, st, keys, tmp);
+    // local partition rounds (segments of kUnitMax+1 .. kLocalMax keys)
+    int lc = 0;
+    int rounds = 0;
+    while (!aborted() && h.nlocal[lc] + h.nlocal_big[lc] > 0) {
+        KS_CK(cudaMemsetAsync(&st->local_next, 0, sizeof(int), stream));
+        KS_CK(cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream));
+        KS_CK(cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream));
+        EmitArgs A{segs[0], &st->nseg[0], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1], L.lseg_cap,
+                   units, L.unit_cap};
+        const int nl = h.nlocal[lc] + h.nlocal_big[lc];
+        const int grid = nl < g_local ? nl : g_local;
+        K.run(kPhScatter, [&] {
+            k_local<<<grid, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
+                                                                        L.lseg_cap, A, st, keys, tmp);
         });
-        KS_CK(cudaGetLastError());
-        KS_CK(cudaMemcpyAsync(&h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
-        KS_CK(cudaStreamSynchronize(stream));
+        KS_CK(cudaMemsetAsync(&st->nlocal[lc], 0, sizeof(int), stream));
+        KS_CK(cudaMemsetAsync(&st->nlocal_big[lc], 0, sizeof(int), stream));
+        rc = sync_status();
+        if (rc != KS_OK) return rc;
+        lc ^= 1;
+        ++rounds;
+        if (h.nunits > L.unit_cap / 2) {
+            flush_units();
+            rc = sync_status();
+            if (rc != KS_OK) return rc;
+        }
     }
-    res->levels = level;
+    if (!aborted() && h.nunits > 0) {
+        flush_units();
+        rc = sync_status();
+        if (rc != KS_OK) return rc;
+    }
+    res->levels = level + rounds;
     res->bad_index = h.bad_index == kNoIndex ? -1 : (long long)h.bad_index;
     res->mixed_zero = (h.pos_zero && h.neg_zero) ? 1 : 0;
     res->bytes_moved = h.bytes_moved;

@@ -23,16 +23,17 @@ namespace ks {
 constexpr int kPMax = 511;            // max pivot candidates (first P keys) per global pass
 constexpr int kPMaxPow2 = 512;
 constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (1023)
-constexpr int kLutMax = 2048;         // LUT buckets (pow2 >= 4*P)
+constexpr int kLutMax = 4096;         // LUT buckets (pow2 >= 8*P)
 constexpr int kKeysPerPivot = 64;     // P = len / 64 (capped): gaps average ~64..200 keys
 constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
 constexpr int kCountThreads = 512;
-constexpr int kTile = 8192;           // keys staged in shared memory per scatter step
-constexpr int kPassThreads = 512;     // threads of scatter CTAs (16 keys each per tile)
-constexpr int kLeafMax = 8192;        // S: gaps <= S finish on chip
+constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
+constexpr int kPassThreads = 512;     // threads of scatter CTAs (8 keys each per tile)
+constexpr int kLocalMax = 49152;      // segments <= this are partitioned by one CTA (L2-resident)
+constexpr int kLocalBig = 12288;      // local segments above this are scheduled first (LPT)
 constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
 constexpr int kFillMin = 32;          // equality runs >= this are filled, not scattered
-constexpr int kBigThreads = 512;      // CTA of the big-gap sorter
+constexpr int kLocalThreads = 512;    // CTA of the local partitioner
 constexpr int kUnitWarps = 8;         // warps per CTA of the unit sorter
 
 constexpr unsigned long long kNoIndex = ~0ull;
@@ -50,7 +51,9 @@ struct DevStatus {
     unsigned int neg_zero;            // saw -0.0
     int nseg[2];                      // segment counts of the two level tables
     int nunits;                       // warp work items (unit sorts, fills) of the current pass
-    int nbig;                         // CTA work items (gaps of kUnitMax+1 .. S keys)
+    int nlocal[2];                    // local-partition segments (current round, next round)
+    int nlocal_big[2];                // ... of which > kLocalBig keys (stored from the top of the list)
+    int local_next;                   // dynamic work counter of the local round
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
@@ -77,15 +80,15 @@ struct Seg {
     int piv_off;       // offset into the pivot pool (P+1 slots: +inf sentinel)
     int lut_off;       // offset into the LUT pool (T int2 slots)
     int T;             // LUT buckets (1 = plain binary search)
-    int pad0, pad1;
+    int src;           // local rounds: 0 keys / 1 tmp hold the segment
+    int pad1;
     double lo, scale;  // LUT transform t = clamp((v - lo) * scale, 0, T-1)
 };
 
 // Work item of the on-chip finishing pass.
 //  unit: <= kUnitMax keys (a gap plus its pivot's equality run) sorted by one warp
 //  fill: an equality run written with the pivot value, no read
-//  big:  a gap of kUnitMax+1 .. S keys sorted by one CTA
-enum ItemKind : int { kItemUnit = 0, kItemFill = 1, kItemBig = 2 };
+enum ItemKind : int { kItemUnit = 0, kItemFill = 1 };
 struct Item {
     long long start;
     int len;
@@ -110,40 +113,50 @@ __device__ __forceinline__ bool abort_requested(const DevStatus *st)
 }
 
 // Monotone LUT bucket of v: t(v) non-decreasing in v.  (v - lo) and the product
-// round monotonically; scale is finite and > 0 whenever T > 1 (guarded on the
-// host side of the table build), so no NaN can arise from finite v.
+// round monotonically, the float->int conversion saturates (and maps NaN to 0),
+// and scale is finite and > 0 whenever T > 1 (guarded where the table is
+// built), so the bucket map is monotone on every finite key.
 __device__ __forceinline__ int lut_bucket(double v, double lo, double scale, int T)
 {
     if (T <= 1) return 0;
-    double x = (v - lo) * scale;
-    x = fmin(fmax(x, 0.0), (double)(T - 1));
-    return (int)x;
+    const int x = __double2int_rz((v - lo) * scale);
+    return min(max(x, 0), T - 1);
 }
 
-// Class of v against sorted distinct pivots piv[0..k) (piv[k] = NaN sentinel):
-//   lower = #pivots < v;  class = 2*lower + (v == piv[lower]).
+constexpr int kPivPad = 4;   // NaN slots after the k pivots (branch-free probes read up to piv[a+3])
+
+// LUT entry: a | (b << 16) with a = #pivots in buckets < t, b = #pivots in
+// buckets <= t (k <= kPMax < 65536).
+__device__ __forceinline__ unsigned lut_pack(int a, int b) { return (unsigned)a | ((unsigned)b << 16); }
+
+// Class of v against sorted distinct pivots piv[0..k) (piv[k..k+3] = NaN):
+//   r = #pivots < v;  class = 2*r + (v == piv[r]).
 // Even classes are gaps (open value intervals between pivots, i.e. the
 // unfinished subtrees of the K-sort tree), odd classes are equality runs
 // (the pivot and its copies: K-sort routes them right of the key, where they
-// are already final).  lut[t] = (#pivots in buckets < t, #pivots in buckets <= t)
-// brackets lower for bucket t; two predicated probes resolve it in the common
-// case, a binary search handles crowded buckets.
-__device__ __forceinline__ int classify(double v, const double *piv, const int2 *lut, double lo, double scale,
-                                        int T)
+// are already final).  The bucket's LUT entry gives a <= r <= b, and pivots
+// past b are > v.  Most buckets hold no pivot (T >= 8P), so most keys are
+// classified by one 4-byte shared load; buckets with <= 3 pivots are settled
+// by four independent compares; crowded buckets fall back to binary search.
+// The NaN sentinel compares false both ways, so +/-inf or NaN keys (rejected
+// later by the finiteness gate) still classify in range.
+__device__ __forceinline__ int classify(double v, const double *piv, const unsigned *lut, double lo,
+                                        double scale, int T)
 {
-    const int t = lut_bucket(v, lo, scale, T);
-    const int2 ab = lut[t];
-    int a = ab.x;
-    const int b = ab.y;
-    a += (a < b && piv[a] < v) ? 1 : 0;
-    a += (a < b && piv[a] < v) ? 1 : 0;
-    if (a < b && piv[a] < v) {
-        int hi = b;
-        ++a;
-        while (a < hi) {
-            const int mid = (a + hi) >> 1;
-            if (piv[mid] < v) a = mid + 1; else hi = mid;
-        }
+    const unsigned e = lut[lut_bucket(v, lo, scale, T)];
+    int a = (int)(e & 0xffffu);
+    const int b = (int)(e >> 16);
+    if (a == b) return 2 * a;
+    if (b - a <= 3) {
+        const double p0 = piv[a], p1 = piv[a + 1], p2 = piv[a + 2], p3 = piv[a + 3];
+        const int r = a + (p0 < v) + (p1 < v) + (p2 < v);
+        const int eq = (p0 == v) | (p1 == v) | (p2 == v) | (p3 == v);
+        return 2 * r + eq;
+    }
+    int hi = b;
+    while (a < hi) {
+        const int mid = (a + hi) >> 1;
+        if (piv[mid] < v) a = mid + 1; else hi = mid;
     }
     return 2 * a + (piv[a] == v ? 1 : 0);
 }
