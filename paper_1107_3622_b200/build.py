@@ -41,8 +41,9 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    lib = out or LIB
+    if not force and out is None and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = os.path.join(HERE, "build")
@@ -51,16 +52,21 @@ def build(force: bool = False, verbose: bool = False) -> str:
              f'-DKS_GIT="{_git_rev()}"', *ARCH]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    if os.environ.get("KS_TRACE"):
+        flags += ["-DKS_TRACE"]
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         subprocess.run([nvcc, *flags, "-c", src, "-o", obj], check=True)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     subprocess.run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs], check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    out = None
+    if "--out" in sys.argv:
+        out = sys.argv[sys.argv.index("--out") + 1]
+    print(build(force="--force" in sys.argv or out is not None, verbose="-v" in sys.argv, out=out))

@@ -27,6 +27,23 @@
 
 namespace ks {
 
+#ifdef KS_TRACE
+// optional phase-cycle instrumentation (build with KS_TRACE=1), read via ks_trace_read
+__device__ unsigned long long g_trace[16];
+#define KS_TR_DECL long long tr_t0 = clock64()
+#define KS_TR(slot)                                                                  \
+    do {                                                                             \
+        if (threadIdx.x == 0) {                                                      \
+            long long t1_ = clock64();                                               \
+            atomicAdd(&g_trace[slot], (unsigned long long)(t1_ - tr_t0));            \
+            tr_t0 = t1_;                                                             \
+        }                                                                            \
+    } while (0)
+#else
+#define KS_TR_DECL
+#define KS_TR(slot)
+#endif
+
 constexpr int kScanBlock = 4096;   // count-matrix entries per scan CTA (512 thr x 8)
 constexpr int kScanThreads = 512;
 
@@ -144,34 +161,60 @@ __global__ void k_gate_segments(const double *keys, const long long *off, long l
 // ---------------------------------------------------------------------------
 struct PivotScratch {
     double sp[kPMaxPow2];
+    double sq[kPMaxPow2];
     long long sh[33];
     int sk;
 };
 
+// rank of the o-th output of merge(A = s[g0, g0+size), B = s[g0+size, g0+2size)), A first on ties
+__device__ __forceinline__ double merge_pick(const double *s, int g0, int size, int d)
+{
+    const double *A = s + g0, *B = s + g0 + size;
+    int lo = d - size > 0 ? d - size : 0, hi = d < size ? d : size;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (!(B[d - 1 - mid] < A[mid])) lo = mid + 1; else hi = mid;
+    }
+    const int a = lo, b = d - lo;
+    if (b >= size) return A[a];
+    if (a >= size) return B[b];
+    return (B[b] < A[a]) ? B[b] : A[a];
+}
+
 __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, unsigned *lut, PivotScratch &W,
                              int &k_out, int &T_out, double &lo_out, double &scale_out)
 {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int NP = next_pow2(P) < 32 ? 32 : next_pow2(P);
     __syncthreads();
-    if (wid == 0) {
-        double x[16];
-#pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int i = lane * 16 + r;
-            x[r] = i < P ? seg[i] : CUDART_INF;
-        }
-        warp_bitonic_sort<16>(x);
-#pragma unroll
-        for (int r = 0; r < 16; ++r) W.sp[lane * 16 + r] = x[r];
+    // each warp sorts a 32-key run in registers (shuffle network), then
+    // merge-path passes with one output per thread
+    for (int w = wid; w * 32 < NP; w += nw) {
+        const int i = w * 32 + lane;
+        double x[1] = {i < P ? seg[i] : CUDART_INF};
+        warp_bitonic_sort<1>(x);
+        W.sp[i] = x[0];
     }
     __syncthreads();
+    double *cur = W.sp, *nxt = W.sq;
+    for (int size = 32; size < NP; size <<= 1) {
+        for (int o = threadIdx.x; o < NP; o += blockDim.x) {
+            const int g0 = o & ~(2 * size - 1);
+            nxt[o] = merge_pick(cur, g0, size, o - g0);
+        }
+        __syncthreads();
+        double *t = cur;
+        cur = nxt;
+        nxt = t;
+    }
+    const double *sp = cur;
     long long carry = 0;
     for (int base = 0; base < P; base += blockDim.x) {
         const int i = base + threadIdx.x;
-        const int keep = (i < P && (i == 0 || W.sp[i] != W.sp[i - 1])) ? 1 : 0;
+        const int keep = (i < P && (i == 0 || sp[i] != sp[i - 1])) ? 1 : 0;
         long long tot;
         const long long pos = block_exclusive_scan(keep, W.sh, &tot);
-        if (keep) piv[carry + pos] = W.sp[i];
+        if (keep) piv[carry + pos] = sp[i];
         carry += tot;
     }
     const int k = (int)carry;
@@ -191,19 +234,36 @@ __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, un
     __syncthreads();
     for (int j = threadIdx.x; j < k; j += blockDim.x) atomicAdd(&lut[lut_bucket(piv[j], lo, scale, T)], 1u);
     __syncthreads();
-    {   // exclusive scan over T buckets, T / blockDim consecutive buckets per thread
-        const int per = (T + blockDim.x - 1) / blockDim.x;
-        const int t0 = threadIdx.x * per;
-        int local = 0;
-        for (int q = 0; q < per; ++q)
-            if (t0 + q < T) local += (int)lut[t0 + q];
-        long long ex = block_exclusive_scan(local, W.sh, nullptr);
-        for (int q = 0; q < per; ++q) {
-            if (t0 + q < T) {
-                const int c = (int)lut[t0 + q];
-                lut[t0 + q] = lut_pack((int)ex, (int)ex + c);
-                ex += c;
+    {   // exclusive scan over T buckets: warp w owns a contiguous slice, scanned 32 at a time
+        const int per_w = (T + nw - 1) / nw;
+        const int b0 = wid * per_w, b1 = min(T, b0 + per_w);
+        int run = 0;
+        for (int base = b0; base < b1; base += 32) {
+            const int t = base + lane;
+            const int c = t < b1 ? (int)lut[t] : 0;
+            int inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
             }
+            if (t < b1) lut[t] = (unsigned)(run + inc - c);   // exclusive within the warp's slice
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) W.sh[wid] = run;
+        __syncthreads();
+        int wbase = 0;
+        for (int q = 0; q < wid; ++q) wbase += (int)W.sh[q];
+        for (int base = b0; base < b1; base += 32) {   // warp-uniform trip count
+            const int t = base + lane;
+            int a = 0, nxt = 0;
+            if (t < b1) {
+                a = wbase + (int)lut[t];
+                nxt = (t + 1 < b1) ? wbase + (int)lut[t + 1] : wbase + run;
+            }
+            __syncwarp();   // all reads of this row before any lane overwrites its entry
+            if (t < b1) lut[t] = lut_pack(a, nxt);
+            __syncwarp();
         }
     }
     __syncthreads();
@@ -447,30 +507,30 @@ __device__ __forceinline__ long long class_start(const Seg &g, const long long *
 }
 
 // ---------------------------------------------------------------------------
-// scatter: classify again, rank each key inside its tile (shared atomics),
-// group the tile by class in shared memory, then write each class's run
-// contiguously to its destination (coalesced runs).  Equality runs of at
-// least kFillMin keys are not written: the finishing pass fills them.
+// scatter: classify again and send each key straight to its class slot:
+// slot = atomicAdd(cursor[class]) on a shared-memory cursor seeded with the
+// chunk's offset from the scanned count matrix (32-bit, relative to the
+// segment start).  No tile staging: on B200 the direct 8-byte scatter into
+// the L2-resident destination costs fewer shared-memory wavefronts than
+// staging runs (ncu: staged 1.56 wavefronts/key, smem-bound).  Equality
+// runs of at least kFillMin keys are not written: the finish pass fills them.
 // ---------------------------------------------------------------------------
 struct ScatterSmem {
-    double stage[kTile];
-    long long sdst[kTile];     // destination of each staged key (-1: equality run that is filled later)
-    long long cur[kRowsMax];   // class cursors; LLONG_MIN marks classes that are not written
     PassSmem P;
-    unsigned hist[kRowsMax + 1];
-    unsigned off[kRowsMax + 1];
-    long long sh[33];
+    unsigned cursor[kRowsMax + 1];   // next slot per class, relative to the segment start
+    unsigned char skip[kRowsMax + 1];
     Seg sg;
 };
 
-__global__ void __launch_bounds__(kPassThreads, 2) k_scatter(const Seg *segs, const int *chunk_seg,
-                                                             const DevStatus *cst, const double *src, double *dst,
-                                                             const double *piv_pool, const unsigned *lut_pool,
-                                                             const long long *moff)
+__global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const int *chunk_seg,
+                                                          const DevStatus *cst, const double *src, double *dst,
+                                                          const double *piv_pool, const unsigned *lut_pool,
+                                                          const long long *moff)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
-    constexpr int E = kTile / kPassThreads;   // keys per thread per tile (8)
+    constexpr int U = 8;
+    if (abort_requested(cst)) return;   // non-finite key or both signed zeros: write nothing
     int cached = -1;
     const int nchunks = cst->nchunks;
     for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
@@ -490,67 +550,27 @@ __global__ void __launch_bounds__(kPassThreads, 2) k_scatter(const Seg *segs, co
         for (int c = threadIdx.x; c < rows; c += blockDim.x) {
             const long long c0 = class_start(g, moff, base_i, c);
             const long long tot = class_start(g, moff, base_i, c + 1) - c0;
-            const bool skip = (c & 1) && tot >= kFillMin;   // long equality run: filled by the finish pass
-            S.cur[c] = skip ? LLONG_MIN : g.start + (moff[g.mat_off + (long long)c * nch + j] - base_i);
+            S.skip[c] = ((c & 1) && tot >= kFillMin) ? 1 : 0;   // long equality run: filled by the finish pass
+            S.cursor[c] = (unsigned)(moff[g.mat_off + (long long)c * nch + j] - base_i);
         }
-        const double *in = src + base;
-        for (int t0 = 0; t0 < cnt; t0 += kTile) {
-            const int tcnt = min(kTile, cnt - t0);
-            for (int c = threadIdx.x; c < rows; c += blockDim.x) S.hist[c] = 0;
-            __syncthreads();
-            double v[E];
-            unsigned cl[E], rk[E];
-            if (tcnt == kTile) {
+        __syncthreads();
+        const double *in = src + base + threadIdx.x;
+        double *out = dst + g.start;
+        int i0 = 0;
+        for (; i0 + U * kPassThreads <= cnt; i0 += U * kPassThreads) {
+            double v[U];
 #pragma unroll
-                for (int e = 0; e < E; ++e) v[e] = in[t0 + e * kPassThreads + threadIdx.x];
+            for (int u = 0; u < U; ++u) v[u] = in[i0 + u * kPassThreads];
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    cl[e] = (unsigned)classify(v[e], S.P.piv, S.P.lut, lo, scale, T);
-                    rk[e] = atomicAdd(&S.hist[cl[e]], 1u);
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    const int i = e * kPassThreads + threadIdx.x;
-                    v[e] = i < tcnt ? in[t0 + i] : 0.0;
-                    if (i < tcnt) {
-                        cl[e] = (unsigned)classify(v[e], S.P.piv, S.P.lut, lo, scale, T);
-                        rk[e] = atomicAdd(&S.hist[cl[e]], 1u);
-                    }
-                }
+            for (int u = 0; u < U; ++u) {
+                const int c = classify(v[u], S.P.piv, S.P.lut, lo, scale, T);
+                if (!S.skip[c]) out[atomicAdd(&S.cursor[c], 1u)] = v[u];
             }
-            __syncthreads();
-            {   // exclusive scan of the tile histogram: 2 classes per thread
-                const int c0 = 2 * threadIdx.x;
-                const unsigned h0 = c0 < rows ? S.hist[c0] : 0u;
-                const unsigned h1 = c0 + 1 < rows ? S.hist[c0 + 1] : 0u;
-                const long long ex = block_exclusive_scan((long long)h0 + h1, S.sh, nullptr);
-                if (c0 < rows) S.off[c0] = (unsigned)ex;
-                if (c0 + 1 < rows) S.off[c0 + 1] = (unsigned)ex + h0;
-            }
-            __syncthreads();
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int i = e * kPassThreads + threadIdx.x;
-                if (i < tcnt) {
-                    const unsigned p = S.off[cl[e]] + rk[e];
-                    const long long cb = S.cur[cl[e]];
-                    S.stage[p] = v[e];
-                    S.sdst[p] = cb < 0 ? -1 : cb + rk[e];
-                }
-            }
-            __syncthreads();
-#pragma unroll
-            for (int e = 0; e < E; ++e) {
-                const int p = e * kPassThreads + threadIdx.x;
-                if (p < tcnt) {
-                    const long long d = S.sdst[p];
-                    if (d >= 0) dst[d] = S.stage[p];
-                }
-            }
-            __syncthreads();
-            for (int c = threadIdx.x; c < rows; c += blockDim.x)
-                if (S.cur[c] >= 0) S.cur[c] += S.hist[c];
+        }
+        for (int i = i0 + threadIdx.x; i < cnt; i += kPassThreads) {
+            const double v = src[base + i];
+            const int c = classify(v, S.P.piv, S.P.lut, lo, scale, T);
+            if (!S.skip[c]) out[atomicAdd(&S.cursor[c], 1u)] = v;
         }
     }
 }
@@ -603,11 +623,13 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     if (have && el >= kFillMin) f_eq = 1;
     else if (have && eq_written && !eq_packed && dst_id == 1) u_eq = 1;
     const int nu = u_gap + u_eq + f_eq;
-    long long tu, tl, tlb, tg;
-    const long long xu = block_exclusive_scan(nu, sh, &tu);
-    const long long xl = block_exclusive_scan(l_gap, sh, &tl);
-    const long long xlb = block_exclusive_scan(lb_gap, sh, &tlb);
-    const long long xg = block_exclusive_scan(g_gap, sh, &tg);
+    // one packed scan for the four list counts (each block total <= 3 * 512 < 2^16)
+    const long long pk = (long long)nu | ((long long)l_gap << 16) | ((long long)lb_gap << 32) |
+                         ((long long)g_gap << 48);
+    long long tpk;
+    const long long xpk = block_exclusive_scan(pk, sh, &tpk);
+    const long long xu = xpk & 0xffff, xl = (xpk >> 16) & 0xffff, xlb = (xpk >> 32) & 0xffff, xg = (xpk >> 48) & 0xffff;
+    const long long tu = tpk & 0xffff, tl = (tpk >> 16) & 0xffff, tlb = (tpk >> 32) & 0xffff, tg = (tpk >> 48) & 0xffff;
     if (threadIdx.x == 0) {
         sbase[0] = tu ? atomicAdd(&st->nunits, (int)tu) : 0;
         sbase[1] = tl ? atomicAdd(A.nlnext, (int)tl) : 0;
@@ -641,9 +663,10 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         const long long gi = sbase[2] + xg;
         if (gi < A.gcap) A.gnext[gi] = make_seg(ag, gl, dst_id); else st->overflow = 4;
     }
-    long long t_fk, t_uk;
-    block_exclusive_scan(f_eq ? el : 0, sh, &t_fk);
-    block_exclusive_scan((u_gap ? ulen_gap : 0) + (u_eq ? el : 0), sh, &t_uk);
+    // keys in fills / units (block totals; segments < 2^31 keys)
+    long long tk;
+    block_exclusive_scan((f_eq ? el : 0) | (((u_gap ? ulen_gap : 0) + (u_eq ? el : 0)) << 32), sh, &tk);
+    const long long t_fk = tk & 0xffffffffll, t_uk = tk >> 32;
     EmitOut o;
     o.unit_keys = t_uk;
     o.fill_keys = t_fk;
@@ -674,6 +697,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
 {
     __shared__ long long sh[33];
     __shared__ long long sbase[4];
+    if (abort_requested(st)) return;
     const int ns = *nseg;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
         __syncthreads();
@@ -721,6 +745,7 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LocalSmem &L = *reinterpret_cast<LocalSmem *>(smem_raw);
+    if (abort_requested(st)) return;
     const int nb = *nlocal_big, n = *nlocal + nb;
     for (;;) {
         __syncthreads();
@@ -737,7 +762,9 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
         const int P = pivots_for(m);
         int k, T;
         double lo, scale;
+        KS_TR_DECL;
         build_pivots(src, P, lut_for(P), L.piv, L.lut, L.W, k, T, lo, scale);
+        KS_TR(0);
         const int rows = 2 * k + 1;
         for (int c = threadIdx.x; c < rows; c += blockDim.x) L.hist[c] = 0;
         __syncthreads();
@@ -753,6 +780,7 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
         for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads)
             atomicAdd(&L.hist[classify(src[i], L.piv, L.lut, lo, scale, T)], 1u);
         __syncthreads();
+        KS_TR(1);
         {   // exclusive scan of the class histogram -> class starts (2 classes per thread)
             const int c0 = 2 * threadIdx.x;
             const unsigned h0 = c0 < rows ? L.hist[c0] : 0u;
@@ -779,6 +807,7 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
             if (!(c & 1) || L.hist[c] < (unsigned)kFillMin) dst[atomicAdd(&L.cursor[c], 1u)] = v;
         }
         __syncthreads();
+        KS_TR(2);
         // class starts = cursor - (keys written); emit per pivot pair
         const int j = threadIdx.x;
         const bool have = j <= k;
@@ -795,6 +824,10 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
         }
         const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase);
         if (threadIdx.x == 0) account_partition(st, g.len, o);
+        KS_TR(3);
+#ifdef KS_TRACE
+        if (threadIdx.x == 0) { atomicAdd(&g_trace[4], 1ull); atomicAdd(&g_trace[5], (unsigned long long)m); }
+#endif
     }
 }
 
@@ -964,9 +997,10 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
     L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
     L.mat_cap = (2 * psum + L.seg_cap) + (long long)(2 * kPMax + 1) * (2 * (n / kChunk) + 2);
-    // finishing items emitted by one round <= 2 per pivot + 1 per segment; the list is
-    // flushed whenever it is more than half full, so twice that bound suffices
-    L.unit_cap = (int)(2 * (2 * (n / kKeysPerPivot) + 3 * (long long)L.lseg_cap + 2 * L.seg_cap) + 4096);
+    // finishing items emitted by one round <= 2 per pivot + 1 per segment; later the list
+    // is flushed whenever it is more than half full
+    // (the speculative schedule runs up to four partition rounds before the first flush)
+    L.unit_cap = (int)(4 * (2 * (n / kKeysPerPivot) + 3 * (long long)L.lseg_cap + 2 * L.seg_cap) + 4096);
     L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
     size_t off = 0;
     L.o_status = off; off = align_up(off + sizeof(DevStatus));
@@ -1048,77 +1082,75 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         });
         K.run(kPhGate, [&] { k_gate_segments<<<sms * 4, 256, 0, stream>>>(keys, d_off, nseg0, 0, st); });
     }
-    int rc = sync_status();
-    if (rc != KS_OK) return rc;
 
-    // global passes (segments > kLocalMax)
-    int level = 0;
-    int cur = 0;
-    while (h.nseg[cur] > 0 && !aborted()) {
+    // The schedule is launched speculatively without host round-trips: global
+    // passes and local rounds read their work counts on the device and exit
+    // at once when empty.  One status read at the end; inputs that need more
+    // passes (adversarial shapes: presorted, few distinct values, ...) continue
+    // in a synchronising loop.
+    int level = 0, gcur = 0, rounds = 0, lc = 0;
+    auto global_pass = [&]() {
         const double *src = (level & 1) ? tmp : keys;
         double *dst = (level & 1) ? keys : tmp;
         const int dst_id = (level & 1) ? 0 : 1;
-        int *nseg_cur = &st->nseg[cur];
-        int *nseg_next = &st->nseg[cur ^ 1];
-        EmitArgs A{segs[cur ^ 1], nseg_next, L.seg_cap, lsegs[0], &st->nlocal[0], &st->nlocal_big[0], L.lseg_cap, units,
-                   L.unit_cap};
-        K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[cur], nseg_cur); });
+        int *nseg_cur = &st->nseg[gcur];
+        int *nseg_next = &st->nseg[gcur ^ 1];
+        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
+                   units, L.unit_cap};
+        K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur); });
         K.run(kPhPivots, [&] {
-            k_seg_offsets<<<1, 1024, 0, stream>>>(segs[cur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
+            k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
         });
-        K.run(kPhPivots, [&] { k_pivots<<<g_seg, 256, 0, stream>>>(segs[cur], nseg_cur, src, piv, lut, chunk_seg); });
+        K.run(kPhPivots, [&] { k_pivots<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg); });
         if (level == 0)
             K.run(kPhCount, [&] {
-                k_count<true><<<g_count, kCountThreads, 0, stream>>>(segs[cur], chunk_seg, st, src, piv, lut, mat, st);
+                k_count<true><<<g_count, kCountThreads, 0, stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
         else
             K.run(kPhCount, [&] {
-                k_count<false><<<g_count, kCountThreads, 0, stream>>>(segs[cur], chunk_seg, st, src, piv, lut, mat, st);
+                k_count<false><<<g_count, kCountThreads, 0, stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
         K.run(kPhScan, [&] { k_scan_reduce<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum); });
         K.run(kPhScan, [&] { k_scan_bsums<<<1, 1024, 0, stream>>>(bsum, st); });
         K.run(kPhScan, [&] { k_scan_apply<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum, moff); });
         K.run(kPhScatter, [&] {
-            k_scatter<<<g_scatter, kPassThreads, sizeof(ScatterSmem), stream>>>(segs[cur], chunk_seg, st, src, dst, piv,
+            k_scatter<<<g_scatter, kPassThreads, sizeof(ScatterSmem), stream>>>(segs[gcur], chunk_seg, st, src, dst, piv,
                                                                                lut, moff);
         });
-        KS_CK(cudaMemsetAsync(nseg_next, 0, sizeof(int), stream));
-        K.run(kPhPlan, [&] { k_plan<<<g_seg, kPlanThreads, 0, stream>>>(segs[cur], nseg_cur, piv, moff, A, st, dst_id); });
-        rc = sync_status();
-        if (rc != KS_OK) return rc;
+        cudaMemsetAsync(nseg_next, 0, sizeof(int), stream);
+        K.run(kPhPlan, [&] { k_plan<<<g_seg, kPlanThreads, 0, stream>>>(segs[gcur], nseg_cur, piv, moff, A, st, dst_id); });
+        cudaMemsetAsync(nseg_cur, 0, sizeof(int), stream);
         ++level;
-        cur ^= 1;
-        if (!aborted() && h.nunits > L.unit_cap / 2) flush_units();
-    }
-    // local partition rounds (segments of kUnitMax+1 .. kLocalMax keys)
-    int lc = 0;
-    int rounds = 0;
-    while (!aborted() && h.nlocal[lc] + h.nlocal_big[lc] > 0) {
-        KS_CK(cudaMemsetAsync(&st->local_next, 0, sizeof(int), stream));
-        KS_CK(cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream));
-        KS_CK(cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream));
-        EmitArgs A{segs[0], &st->nseg[0], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1], L.lseg_cap,
-                   units, L.unit_cap};
-        const int nl = h.nlocal[lc] + h.nlocal_big[lc];
-        const int grid = nl < g_local ? nl : g_local;
+        gcur ^= 1;
+    };
+    auto local_round = [&]() {
+        cudaMemsetAsync(&st->local_next, 0, sizeof(int), stream);
+        cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream);
+        cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
+        EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
+                   L.lseg_cap, units, L.unit_cap};
         K.run(kPhScatter, [&] {
-            k_local<<<grid, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
-                                                                        L.lseg_cap, A, st, keys, tmp);
+            k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
+                                                                           L.lseg_cap, A, st, keys, tmp);
         });
-        KS_CK(cudaMemsetAsync(&st->nlocal[lc], 0, sizeof(int), stream));
-        KS_CK(cudaMemsetAsync(&st->nlocal_big[lc], 0, sizeof(int), stream));
-        rc = sync_status();
-        if (rc != KS_OK) return rc;
+        cudaMemsetAsync(&st->nlocal[lc], 0, sizeof(int), stream);
+        cudaMemsetAsync(&st->nlocal_big[lc], 0, sizeof(int), stream);
         lc ^= 1;
         ++rounds;
-        if (h.nunits > L.unit_cap / 2) {
-            flush_units();
-            rc = sync_status();
-            if (rc != KS_OK) return rc;
-        }
-    }
-    if (!aborted() && h.nunits > 0) {
-        flush_units();
+    };
+    // speculative part: expected shape of a random input
+    const int spec_global = n > kLocalMax ? (n > 4 * 1048576 ? 2 : 1) : 0;
+    for (int i = 0; i < spec_global; ++i) global_pass();
+    local_round();
+    local_round();
+    flush_units();
+    int rc = sync_status();
+    if (rc != KS_OK) return rc;
+    // remaining work (rare): finish with host checks
+    while (!aborted() && (h.nseg[gcur] > 0 || h.nlocal[lc] + h.nlocal_big[lc] > 0 || h.nunits > 0)) {
+        if (h.nseg[gcur] > 0) global_pass();
+        else if (h.nlocal[lc] + h.nlocal_big[lc] > 0) local_round();
+        if (h.nunits > L.unit_cap / 2 || (h.nseg[gcur] == 0 && h.nlocal[lc] + h.nlocal_big[lc] == 0)) flush_units();
         rc = sync_status();
         if (rc != KS_OK) return rc;
     }
@@ -1136,3 +1168,17 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 }
 
 }  // namespace ks
+
+#ifdef KS_TRACE
+extern "C" int ks_trace_read(unsigned long long *out, int n, int reset)
+{
+    unsigned long long h[16];
+    cudaMemcpyFromSymbol(h, ks::g_trace, sizeof(h));
+    for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
+    if (reset) {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(ks::g_trace, z, sizeof(z));
+    }
+    return 0;
+}
+#endif
