@@ -50,11 +50,14 @@ __device__ __forceinline__ void warp_bitonic_sort(double (&x)[E])
             }
         }
     }
-    // k = 2E .. 32E: lane-distance stages by shuffle, then in-lane half-cleaners
-#pragma unroll 1
+    // k = 2E .. 32E: lane-distance stages by shuffle, then in-lane half-cleaners.
+    // Small E (the common unit sizes) unroll completely -- rolled loops cost a
+    // divergence check and loop bookkeeping per stage; large E stay rolled to
+    // bound code size (I-cache).
+#pragma unroll (E <= 4 ? 5 : 1)
     for (int kk = 2; kk <= 32; kk <<= 1) {          // k / E
         const bool asc = (lane & kk) == 0 || kk == 32;
-#pragma unroll 1
+#pragma unroll (E <= 4 ? 5 : 1)
         for (int lj = kk >> 1; lj > 0; lj >>= 1) {  // j / E
             const bool keep_min = ((lane & lj) == 0) == asc;
 #pragma unroll

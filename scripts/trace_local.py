@@ -1,4 +1,4 @@
-"""Phase cycles of k_local per segment (needs scripts/libksort_trace.so built with KS_TRACE=1)."""
+"""Phase cycles of k_finish per piece (needs scripts/libksort_trace.so built with KS_TRACE=1)."""
 import ctypes
 import os
 import sys
@@ -23,7 +23,7 @@ for rep in range(3):
     torch.cuda.synchronize()
     L.ks_trace_read(ctypes.addressof(buf), 16, 0)
     segs, keys = buf[4], buf[5]
-    print("rep %d: %d local segments, %d keys; cycles/segment: pivots %.0f count %.0f scatter %.0f emit %.0f; "
-          "cycles/key: count %.2f scatter %.2f" % (rep, segs, keys, buf[0] / max(segs, 1), buf[1] / max(segs, 1),
-                                                    buf[2] / max(segs, 1), buf[3] / max(segs, 1),
-                                                    buf[1] / max(keys, 1), buf[2] / max(keys, 1)))
+    print("rep %d: %d pieces (> 512 keys), %d keys; cycles/piece: load+pivots %.0f classify %.0f scan+perm %.0f "
+          "sort-units %.0f; cycles/key: classify %.2f sort %.2f" % (
+              rep, segs, keys, buf[0] / max(segs, 1), buf[1] / max(segs, 1), buf[2] / max(segs, 1),
+              buf[3] / max(segs, 1), buf[1] / max(keys, 1), buf[3] / max(keys, 1)))
