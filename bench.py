@@ -275,7 +275,7 @@ def run_ours(args):
     prof = _sort_device(keys, _lib.KS_FLAG_PROFILE)
     phase = {nm: {"ms": float(prof.phase_ms[i]), "launches": int(prof.phase_launches[i]),
                   "bytes": int(prof.phase_bytes[i])} for i, nm in enumerate(_lib.PHASES)}
-    dom = max(("count", "scatter", "leaf"), key=lambda k: phase[k]["ms"])
+    dom = max(("count", "scatter", "leaf", "local"), key=lambda k: phase[k]["ms"])
     hbm, peak_kind = peaks()
     dom_gbs = phase[dom]["bytes"] / (phase[dom]["ms"] * 1e-3) / 1e9 if phase[dom]["ms"] > 0 else 0.0
 

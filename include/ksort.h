@@ -58,7 +58,7 @@ typedef struct ks_status {
     int32_t launches;           /* kernels launched by this call */
     /* per-phase telemetry, filled only with KS_FLAG_PROFILE (CUDA events on `stream`):
      * phase 0 gate/init, 1 pivots (segment setup), 2 count, 3 scan, 4 scatter,
-     * 5 plan, 6 leaf (on-chip finish + fills), 7 reserved */
+     * 5 plan, 6 leaf (on-chip finish + fills), 7 local (one-CTA partition rounds) */
     float phase_ms[8];
     int32_t phase_launches[8];
     uint64_t phase_bytes[8];    /* algorithmic bytes of each phase (reads + writes) */

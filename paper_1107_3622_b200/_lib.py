@@ -22,7 +22,7 @@ KS_NEED_EXACT = 6
 KS_FLAG_EXACT = 1
 KS_FLAG_COUNTS = 2
 KS_FLAG_PROFILE = 4
-PHASES = ("gate", "pivots", "count", "scan", "scatter", "plan", "leaf", "other")
+PHASES = ("gate", "pivots", "count", "scan", "scatter", "plan", "leaf", "local")
 
 EXPORTED = (
     "ks_workspace_bytes", "ks_sort_f64", "ks_sort_f64_segmented", "ks_partition_f64",

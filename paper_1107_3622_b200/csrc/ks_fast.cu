@@ -674,12 +674,12 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     return o;
 }
 
-__device__ __forceinline__ void account_partition(DevStatus *st, long long len, const EmitOut &o)
+__device__ __forceinline__ void account_partition(DevStatus *st, long long len, const EmitOut &o, bool local)
 {
     // algorithmic bytes: count reads 8B/key; scatter reads 8B/key and writes 8B
     // per key it places; units read+write 16B/key; fills write 8B/key
-    add_bytes(st, kPhCount, 8ull * len);
-    add_bytes(st, kPhScatter, 8ull * len + 8ull * (len - o.fill_keys));
+    add_bytes(st, local ? kPhOther : kPhCount, 8ull * len);
+    add_bytes(st, local ? kPhOther : kPhScatter, 8ull * len + 8ull * (len - o.fill_keys));
     add_bytes(st, kPhLeaf, 16ull * o.unit_keys + 8ull * o.fill_keys);
     atomicAdd(&st->keys_partitioned, (unsigned long long)len);
     atomicAdd(&st->keys_leaf, (unsigned long long)o.unit_keys);
@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
             }
         }
         const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase);
-        if (threadIdx.x == 0) account_partition(st, g.len, o);
+        if (threadIdx.x == 0) account_partition(st, g.len, o, false);
     }
 }
 
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
             }
         }
         const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase);
-        if (threadIdx.x == 0) account_partition(st, g.len, o);
+        if (threadIdx.x == 0) account_partition(st, g.len, o, true);
         KS_TR(3);
 #ifdef KS_TRACE
         if (threadIdx.x == 0) { atomicAdd(&g_trace[4], 1ull); atomicAdd(&g_trace[5], (unsigned long long)m); }
@@ -1129,7 +1129,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
         EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
                    L.lseg_cap, units, L.unit_cap};
-        K.run(kPhScatter, [&] {
+        K.run(kPhOther, [&] {
             k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
                                                                            L.lseg_cap, A, st, keys, tmp);
         });
