@@ -50,10 +50,11 @@ constexpr int kScanThreads = 512;
 // ---------------------------------------------------------------------------
 // work lists
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ Item make_item(long long start, long long len, int kind, int src)
+__device__ __forceinline__ Item make_item(long long start, long long len, int kind, int src, long long tag = -1)
 {
     Item it{};
     it.start = start;
+    it.tag = tag;
     it.len = (int)len;
     it.kind = kind;
     it.src = src;
@@ -599,10 +600,11 @@ struct EmitArgs {
     int lcap;
     Item *units;
     int ucap;
+    int tag_round;     // pass / round number: makes unit tags unique per partition
 };
 
 __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
-                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase)
+                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase, long long tag)
 {
     const bool eq_written = el > 0 && el < kFillMin;   // the scatter wrote these keys
     int u_gap = 0, l_gap = 0, lb_gap = 0, g_gap = 0, u_eq = 0, f_eq = 0;
@@ -639,7 +641,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     __syncthreads();
     long long ui = sbase[0] + xu;
     if (u_gap) {
-        if (ui < A.ucap) A.units[ui] = make_item(ag, ulen_gap, kItemUnit, dst_id); else st->overflow = 3;
+        if (ui < A.ucap) A.units[ui] = make_item(ag, ulen_gap, kItemUnit, dst_id, tag); else st->overflow = 3;
         ++ui;
     }
     if (u_eq) {
@@ -716,7 +718,8 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
                 pv = piv_pool[g.piv_off + j];
             }
         }
-        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase);
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase,
+                                     (g.start << 8) | (A.tag_round & 0xff));
         if (threadIdx.x == 0) account_partition(st, g.len, o, false);
     }
 }
@@ -822,7 +825,8 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
                 pv = L.piv[j];
             }
         }
-        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase);
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase,
+                                     (g.start << 8) | (A.tag_round & 0xff));
         if (threadIdx.x == 0) account_partition(st, g.len, o, true);
         KS_TR(3);
 #ifdef KS_TRACE
@@ -884,9 +888,9 @@ __global__ void __launch_bounds__(kUnitWarps * 32, 3) k_finish_units(const Item 
         const double *in = (it.src ? tmp : keys) + it.start;
         if (m <= 2) {
             if (lane == 0) {
-                double a = in[0];
+                const double a = in[0];
                 if (m == 2) {
-                    double b = in[1];
+                    const double b = in[1];
                     out[0] = b < a ? b : a;
                     out[1] = b < a ? a : b;
                 } else {
@@ -1096,7 +1100,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         int *nseg_cur = &st->nseg[gcur];
         int *nseg_next = &st->nseg[gcur ^ 1];
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
-                   units, L.unit_cap};
+                   units, L.unit_cap, level};
         K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur); });
         K.run(kPhPivots, [&] {
             k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
@@ -1128,7 +1132,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream);
         cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
         EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
-                   L.lseg_cap, units, L.unit_cap};
+                   L.lseg_cap, units, L.unit_cap, 128 + rounds};
         K.run(kPhOther, [&] {
             k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
                                                                            L.lseg_cap, A, st, keys, tmp);

@@ -91,6 +91,7 @@ struct Seg {
 enum ItemKind : int { kItemUnit = 0, kItemFill = 1 };
 struct Item {
     long long start;
+    long long tag;     // partition id (its segment start): only units of one partition are packed together
     int len;
     int kind;          // ItemKind
     int src;           // 0: keys hold the data, 1: tmp holds the data

@@ -161,4 +161,148 @@ __device__ __forceinline__ unsigned lanemask_lt()
     return m;
 }
 
+// Batcher odd-even merge sort of 16 keys in one thread's registers: 63
+// compare-exchanges, all ascending (comparator list generated from the
+// standard recursive construction; written out so every index is a
+// compile-time register).
+template <int N>
+__device__ __forceinline__ void thread_sort(double (&x)[N]);
+
+template <>
+__device__ __forceinline__ void thread_sort<16>(double (&x)[16])
+{
+    cas(x[0], x[1], true);
+    cas(x[2], x[3], true);
+    cas(x[4], x[5], true);
+    cas(x[6], x[7], true);
+    cas(x[8], x[9], true);
+    cas(x[10], x[11], true);
+    cas(x[12], x[13], true);
+    cas(x[14], x[15], true);
+    cas(x[0], x[2], true);
+    cas(x[1], x[3], true);
+    cas(x[4], x[6], true);
+    cas(x[5], x[7], true);
+    cas(x[8], x[10], true);
+    cas(x[9], x[11], true);
+    cas(x[12], x[14], true);
+    cas(x[13], x[15], true);
+    cas(x[1], x[2], true);
+    cas(x[5], x[6], true);
+    cas(x[9], x[10], true);
+    cas(x[13], x[14], true);
+    cas(x[0], x[4], true);
+    cas(x[1], x[5], true);
+    cas(x[2], x[6], true);
+    cas(x[3], x[7], true);
+    cas(x[8], x[12], true);
+    cas(x[9], x[13], true);
+    cas(x[10], x[14], true);
+    cas(x[11], x[15], true);
+    cas(x[2], x[4], true);
+    cas(x[3], x[5], true);
+    cas(x[10], x[12], true);
+    cas(x[11], x[13], true);
+    cas(x[1], x[2], true);
+    cas(x[3], x[4], true);
+    cas(x[5], x[6], true);
+    cas(x[9], x[10], true);
+    cas(x[11], x[12], true);
+    cas(x[13], x[14], true);
+    cas(x[0], x[8], true);
+    cas(x[1], x[9], true);
+    cas(x[2], x[10], true);
+    cas(x[3], x[11], true);
+    cas(x[4], x[12], true);
+    cas(x[5], x[13], true);
+    cas(x[6], x[14], true);
+    cas(x[7], x[15], true);
+    cas(x[4], x[8], true);
+    cas(x[5], x[9], true);
+    cas(x[6], x[10], true);
+    cas(x[7], x[11], true);
+    cas(x[2], x[4], true);
+    cas(x[3], x[5], true);
+    cas(x[6], x[8], true);
+    cas(x[7], x[9], true);
+    cas(x[10], x[12], true);
+    cas(x[11], x[13], true);
+    cas(x[1], x[2], true);
+    cas(x[3], x[4], true);
+    cas(x[5], x[6], true);
+    cas(x[7], x[8], true);
+    cas(x[9], x[10], true);
+    cas(x[11], x[12], true);
+    cas(x[13], x[14], true);
+}
+
+// Merge path over runs A = s[a0, a0+aLen), B = s[b0, b0+bLen) (sidx layout):
+// number of A elements among the first d outputs, A first on ties.
+__device__ __forceinline__ int merge_path2(const double *s, int a0, int aLen, int b0, int bLen, int d)
+{
+    int lo = d - bLen > 0 ? d - bLen : 0;
+    int hi = d < aLen ? d : aLen;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (!(s[sidx(b0 + d - 1 - mid)] < s[sidx(a0 + mid)])) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Warp merge sort of s[0..m) (sidx layout, m <= 32*IPT) in place: each lane
+// sorts IPT consecutive keys in registers (Batcher network), then merge-path
+// rounds double the sorted run length (runs of IPT, 2*IPT, ... < m).
+template <int IPT>
+__device__ __forceinline__ void warp_merge_sort(double *s, int m)
+{
+    const int lane = threadIdx.x & 31;
+    const int o = lane * IPT;
+    double x[IPT];
+#pragma unroll
+    for (int r = 0; r < IPT; ++r) x[r] = (o + r < m) ? s[sidx(o + r)] : CUDART_INF;
+    thread_sort<IPT>(x);
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < IPT; ++r)
+        if (o + r < m) s[sidx(o + r)] = x[r];
+    __syncwarp();
+    for (int R = IPT; R < m; R <<= 1) {
+        bool write = false;
+        if (o < m) {
+            const int g0 = o & ~(2 * R - 1);
+            const int aLen = min(R, m - g0);
+            const int b0 = g0 + R;
+            const int bLen = min(R, m - b0);
+            if (bLen > 0) {
+                const int d = o - g0;
+                int a = merge_path2(s, g0, aLen, b0, bLen, d);
+                int b = d - a;
+                double va = a < aLen ? s[sidx(g0 + a)] : CUDART_INF;
+                double vb = b < bLen ? s[sidx(b0 + b)] : CUDART_INF;
+#pragma unroll
+                for (int r = 0; r < IPT; ++r) {
+                    const bool takeA = !(vb < va);
+                    x[r] = takeA ? va : vb;
+                    if (takeA) {
+                        ++a;
+                        va = a < aLen ? s[sidx(g0 + a)] : CUDART_INF;
+                    } else {
+                        ++b;
+                        vb = b < bLen ? s[sidx(b0 + b)] : CUDART_INF;
+                    }
+                }
+                write = true;
+            }
+        }
+        __syncwarp();
+        if (write) {
+#pragma unroll
+            for (int r = 0; r < IPT; ++r)
+                if (o + r < m) s[sidx(o + r)] = x[r];
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace ks
