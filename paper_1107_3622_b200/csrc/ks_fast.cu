@@ -70,43 +70,54 @@ __device__ __forceinline__ Seg make_seg(long long start, long long len, int src)
     return g;
 }
 
+// Initial work lists (the first global / local round's tables).
+struct InitLists {
+    Seg *gsegs, *lsegs, *ssegs;
+    Item *units;
+    int seg_cap, lseg_cap, sseg_cap, unit_cap;
+};
+
 // Route one segment at start: > kLocalMax keys -> global pass list,
-// kUnitMax < len <= kLocalMax -> local-partition list, 2..kUnitMax -> unit.
-__device__ __forceinline__ void route_initial(long long a, long long len, Seg *gsegs, Seg *lsegs, Item *units,
-                                              DevStatus *st, int seg_cap, int lseg_cap, int unit_cap)
+// kSortMax < len <= kLocalMax -> local-partition list, kUnitMax < len <=
+// kSortMax -> segment sorter, 2..kUnitMax -> unit.
+__device__ __forceinline__ void route_initial(long long a, long long len, const InitLists &Lst, DevStatus *st)
 {
     if (len > kLocalMax) {
         int i = atomicAdd(&st->nseg[0], 1);
-        if (i < seg_cap) gsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
+        if (i < Lst.seg_cap) Lst.gsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
     } else if (len > kLocalBig) {
         int i = atomicAdd(&st->nlocal_big[0], 1);
-        if (i < lseg_cap) lsegs[lseg_cap - 1 - i] = make_seg(a, len, 0); else st->overflow = 1;
-    } else if (len > kUnitMax) {
+        if (i < Lst.lseg_cap) Lst.lsegs[Lst.lseg_cap - 1 - i] = make_seg(a, len, 0); else st->overflow = 1;
+    } else if (len > kSortMax) {
         int i = atomicAdd(&st->nlocal[0], 1);
-        if (i < lseg_cap) lsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
+        if (i < Lst.lseg_cap) Lst.lsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
+    } else if (len > kSortBig) {
+        int i = atomicAdd(&st->nsort_big, 1);
+        if (i < Lst.sseg_cap) Lst.ssegs[Lst.sseg_cap - 1 - i] = make_seg(a, len, 0); else st->overflow = 1;
+    } else if (len > kUnitMax) {
+        int i = atomicAdd(&st->nsort, 1);
+        if (i < Lst.sseg_cap) Lst.ssegs[i] = make_seg(a, len, 0); else st->overflow = 1;
     } else if (len >= 2) {
         int i = atomicAdd(&st->nunits, 1);
-        if (i < unit_cap) units[i] = make_item(a, len, kItemUnit, 0); else st->overflow = 1;
+        if (i < Lst.unit_cap) Lst.units[i] = make_item(a, len, kItemUnit, 0); else st->overflow = 1;
         atomicAdd(&st->keys_leaf, (unsigned long long)len);
         atomicAdd(&st->leaves, 1ull);
         add_bytes(st, kPhLeaf, 16ull * (unsigned long long)len);
     }
 }
 
-__global__ void k_init_single(long long n, Seg *gsegs, Seg *lsegs, Item *units, DevStatus *st, int seg_cap,
-                              int lseg_cap, int unit_cap)
+__global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
 {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    route_initial(0, n, gsegs, lsegs, units, st, seg_cap, lseg_cap, unit_cap);
+    route_initial(0, n, Lst, st);
 }
 
-__global__ void k_init_segmented(const long long *off, long long nseg0, Seg *gsegs, Seg *lsegs, Item *units,
-                                 DevStatus *st, int seg_cap, int lseg_cap, int unit_cap)
+__global__ void k_init_segmented(const long long *off, long long nseg0, InitLists Lst, DevStatus *st)
 {
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nseg0;
          s += (long long)gridDim.x * blockDim.x) {
         const long long a = off[s], b = off[s + 1];
-        route_initial(a, b - a, gsegs, lsegs, units, st, seg_cap, lseg_cap, unit_cap);
+        route_initial(a, b - a, Lst, st);
     }
 }
 
@@ -598,54 +609,53 @@ struct EmitArgs {
     int *nlnext;       // small local segments, stored from index 0 upwards
     int *nlnext_big;   // big local segments (> kLocalBig), stored from index lcap-1 downwards
     int lcap;
+    Seg *snext;        // segment-sorter list
+    int *nsnext;       // <= kSortBig keys, from index 0 upwards
+    int *nsnext_big;   // > kSortBig keys, from index scap-1 downwards
+    int scap;
     Item *units;
     int ucap;
     int tag_round;     // pass / round number: makes unit tags unique per partition
 };
 
+// packed per-thread list counts for one block scan: units (<= 2 per thread,
+// 11 bits) and five 0/1 list flags (10 bits each; blocks have <= 512 threads)
+constexpr int kPkU = 0, kPkS = 11, kPkSB = 21, kPkL = 31, kPkLB = 41, kPkG = 51;
+__device__ __forceinline__ long long pk_get(long long x, int sh, int bits) { return (x >> sh) & ((1ll << bits) - 1); }
+
 __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
                               const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase, long long tag)
 {
-    const bool eq_written = el > 0 && el < kFillMin;   // the scatter wrote these keys
-    int u_gap = 0, l_gap = 0, lb_gap = 0, g_gap = 0, u_eq = 0, f_eq = 0;
-    long long ulen_gap = gl;
+    // every equality run (class 2j+1) is final: it is written as a fill of the pivot value
+    int u_gap = 0, s_gap = 0, sb_gap = 0, l_gap = 0, lb_gap = 0, g_gap = 0;
     if (have && (gl >= 2 || (gl == 1 && dst_id == 1))) {
-        if (gl <= kUnitMax) {
-            u_gap = 1;
-            if (eq_written && gl + el <= kUnitMax) ulen_gap += el;
-        } else if (gl <= kLocalBig) {
-            l_gap = 1;
-        } else if (gl <= kLocalMax) {
-            lb_gap = 1;
-        } else {
-            g_gap = 1;
-        }
+        if (gl <= kUnitMax) u_gap = 1;
+        else if (gl <= kSortBig) s_gap = 1;
+        else if (gl <= kSortMax) sb_gap = 1;
+        else if (gl <= kLocalBig) l_gap = 1;
+        else if (gl <= kLocalMax) lb_gap = 1;
+        else g_gap = 1;
     }
-    const bool eq_packed = u_gap && ulen_gap > gl;
-    if (have && el >= kFillMin) f_eq = 1;
-    else if (have && eq_written && !eq_packed && dst_id == 1) u_eq = 1;
-    const int nu = u_gap + u_eq + f_eq;
-    // one packed scan for the four list counts (each block total <= 3 * 512 < 2^16)
-    const long long pk = (long long)nu | ((long long)l_gap << 16) | ((long long)lb_gap << 32) |
-                         ((long long)g_gap << 48);
+    const int f_eq = (have && el > 0) ? 1 : 0;
+    const int nu = u_gap + f_eq;
+    const long long pk = ((long long)nu << kPkU) | ((long long)s_gap << kPkS) | ((long long)sb_gap << kPkSB) |
+                         ((long long)l_gap << kPkL) | ((long long)lb_gap << kPkLB) | ((long long)g_gap << kPkG);
     long long tpk;
     const long long xpk = block_exclusive_scan(pk, sh, &tpk);
-    const long long xu = xpk & 0xffff, xl = (xpk >> 16) & 0xffff, xlb = (xpk >> 32) & 0xffff, xg = (xpk >> 48) & 0xffff;
-    const long long tu = tpk & 0xffff, tl = (tpk >> 16) & 0xffff, tlb = (tpk >> 32) & 0xffff, tg = (tpk >> 48) & 0xffff;
     if (threadIdx.x == 0) {
-        sbase[0] = tu ? atomicAdd(&st->nunits, (int)tu) : 0;
-        sbase[1] = tl ? atomicAdd(A.nlnext, (int)tl) : 0;
-        sbase[2] = tg ? atomicAdd(A.ngnext, (int)tg) : 0;
-        sbase[3] = tlb ? atomicAdd(A.nlnext_big, (int)tlb) : 0;
+        const int tu = (int)pk_get(tpk, kPkU, 11), ts = (int)pk_get(tpk, kPkS, 10), tsb = (int)pk_get(tpk, kPkSB, 10);
+        const int tl = (int)pk_get(tpk, kPkL, 10), tlb = (int)pk_get(tpk, kPkLB, 10), tg = (int)pk_get(tpk, kPkG, 10);
+        sbase[0] = tu ? atomicAdd(&st->nunits, tu) : 0;
+        sbase[1] = tl ? atomicAdd(A.nlnext, tl) : 0;
+        sbase[2] = tg ? atomicAdd(A.ngnext, tg) : 0;
+        sbase[3] = tlb ? atomicAdd(A.nlnext_big, tlb) : 0;
+        sbase[4] = ts ? atomicAdd(A.nsnext, ts) : 0;
+        sbase[5] = tsb ? atomicAdd(A.nsnext_big, tsb) : 0;
     }
     __syncthreads();
-    long long ui = sbase[0] + xu;
+    long long ui = sbase[0] + pk_get(xpk, kPkU, 11);
     if (u_gap) {
-        if (ui < A.ucap) A.units[ui] = make_item(ag, ulen_gap, kItemUnit, dst_id, tag); else st->overflow = 3;
-        ++ui;
-    }
-    if (u_eq) {
-        if (ui < A.ucap) A.units[ui] = make_item(ae, el, kItemUnit, dst_id); else st->overflow = 3;
+        if (ui < A.ucap) A.units[ui] = make_item(ag, gl, kItemUnit, dst_id, tag); else st->overflow = 3;
         ++ui;
     }
     if (f_eq) {
@@ -653,26 +663,33 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         it.value = pv;
         if (ui < A.ucap) A.units[ui] = it; else st->overflow = 3;
     }
+    if (s_gap) {
+        const long long i = sbase[4] + pk_get(xpk, kPkS, 10);
+        if (i < A.scap) A.snext[i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
+    }
+    if (sb_gap) {
+        const long long i = A.scap - 1 - (sbase[5] + pk_get(xpk, kPkSB, 10));
+        if (i >= 0) A.snext[i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
+    }
     if (l_gap) {
-        const long long li = sbase[1] + xl;
+        const long long li = sbase[1] + pk_get(xpk, kPkL, 10);
         if (li < A.lcap) A.lnext[li] = make_seg(ag, gl, dst_id); else st->overflow = 4;
     }
     if (lb_gap) {
-        const long long li = A.lcap - 1 - (sbase[3] + xlb);
+        const long long li = A.lcap - 1 - (sbase[3] + pk_get(xpk, kPkLB, 10));
         if (li >= 0) A.lnext[li] = make_seg(ag, gl, dst_id); else st->overflow = 4;
     }
     if (g_gap) {
-        const long long gi = sbase[2] + xg;
+        const long long gi = sbase[2] + pk_get(xpk, kPkG, 10);
         if (gi < A.gcap) A.gnext[gi] = make_seg(ag, gl, dst_id); else st->overflow = 4;
     }
     // keys in fills / units (block totals; segments < 2^31 keys)
     long long tk;
-    block_exclusive_scan((f_eq ? el : 0) | (((u_gap ? ulen_gap : 0) + (u_eq ? el : 0)) << 32), sh, &tk);
-    const long long t_fk = tk & 0xffffffffll, t_uk = tk >> 32;
+    block_exclusive_scan((f_eq ? el : 0) | ((u_gap ? gl : 0) << 32), sh, &tk);
     EmitOut o;
-    o.unit_keys = t_uk;
-    o.fill_keys = t_fk;
-    o.items = tu;
+    o.unit_keys = tk >> 32;
+    o.fill_keys = tk & 0xffffffffll;
+    o.items = pk_get(tpk, kPkU, 11);
     return o;
 }
 
@@ -698,7 +715,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
                                                        const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
 {
     __shared__ long long sh[33];
-    __shared__ long long sbase[4];
+    __shared__ long long sbase[6];
     if (abort_requested(st)) return;
     const int ns = *nseg;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
@@ -738,7 +755,7 @@ struct LocalSmem {
     unsigned hist[kRowsMax + 1];
     unsigned cursor[kRowsMax + 1];
     long long sh[33];
-    long long sbase[4];
+    long long sbase[6];
     int item;
 };
 
@@ -912,6 +929,227 @@ __global__ void __launch_bounds__(kUnitWarps * 32, 3) k_finish_units(const Item 
 }
 
 // ---------------------------------------------------------------------------
+// segment sorter: one CTA sorts one whole segment (kUnitMax < len <=
+// kSortMax) on chip and writes it to its final place in the user buffer.
+//   1. the segment is read once, coalesced, into registers (kSortPer keys
+//      per thread); block min / max
+//   2. interpolation buckets b(v) = (v - min) * B / (max - min), B ~ len / 2:
+//      the map is monotone in v (see lut_bucket), so bucket order is value
+//      order; shared-memory histogram, scan, scatter into the staging buffer
+//   3. buckets of <= kThreadSortMax keys: insertion sort by one thread;
+//      larger ones: constant-run check, then a warp bitonic network
+//      (<= kUnitMax keys); larger non-constant buckets (skewed data) are
+//      handed back to the local partitioner, whose first-key pivots do not
+//      depend on the value distribution
+//   4. coalesced write-back.
+// ---------------------------------------------------------------------------
+template <int kT, int kCap>
+struct SortSmem {
+    static constexpr int kBuckets = kCap / kSortLambda;     // interpolation buckets
+    static constexpr int kPB = kBuckets / kT;               // buckets per thread in the scan
+    static constexpr int kBigCap = kCap / (kThreadSortMax + 1) + 1;
+    double a[kCap];        // the segment as loaded
+    double b[kCap];        // bucket order, sorted in place
+    unsigned cur[kBuckets];
+    int big[kBigCap];
+    double red[2][32];
+    long long sh[33];
+    int nbig;
+    int item;
+};
+
+__device__ __forceinline__ int sort_bucket(double v, double lo, double scale, int B)
+{
+    const int x = __double2int_rz((v - lo) * scale);
+    return min(max(x, 0), B - 1);
+}
+
+__device__ __forceinline__ void smem_insertion_sort(double *a, int s)
+{
+    for (int i = 1; i < s; ++i) {
+        const double x = a[i];
+        int j = i - 1;
+        double y = a[j];
+        while (y > x) {
+            a[j + 1] = y;
+            if (--j < 0) break;
+            y = a[j];
+        }
+        a[j + 1] = x;
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void warp_sort_inplace(double *a, int s)
+{
+    const int lane = threadIdx.x & 31;
+    double x[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int i = lane * E + r;
+        x[r] = i < s ? a[i] : CUDART_INF;
+    }
+    warp_bitonic_sort<E>(x);
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+        const int i = lane * E + r;
+        if (i < s) a[i] = x[r];
+    }
+}
+
+// One warp sorts one bucket in place; false if the bucket is too large (and
+// not constant).  Kept out of line: its E = 16 network must not raise the
+// register allocation of the streaming loops around it.
+__device__ __noinline__ bool warp_sort_bucket(double *a, int sz)
+{
+    const int lane = threadIdx.x & 31;
+    const double f = a[0];
+    bool same = true;
+    for (int i = lane; i < sz; i += 32) same &= (a[i] == f);
+    if (__all_sync(0xffffffffu, same)) return true;
+    if (sz <= 32) warp_sort_inplace<1>(a, sz);
+    else if (sz <= 64) warp_sort_inplace<2>(a, sz);
+    else if (sz <= 128) warp_sort_inplace<4>(a, sz);
+    else if (sz <= 256) warp_sort_inplace<8>(a, sz);
+    else if (sz <= kUnitMax) warp_sort_inplace<16>(a, sz);
+    else return false;
+    return true;
+}
+
+// One list of the segment sorter: entries list[dir * d] for d < *count
+// (dir = -1 walks the big-segment half from the top of the array).
+template <int kT, int kCap>
+__global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : 3)
+    k_segsort(const Seg *list, int dir, const int *count, int *next, Seg *lnext, int *nlnext, int lcap,
+              DevStatus *st, double *keys, const double *tmp)
+{
+    using Smem = SortSmem<kT, kCap>;
+    constexpr int kWarps = kT / 32;
+    static_assert(Smem::kPB * kT == Smem::kBuckets, "whole buckets per thread");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
+    if (abort_requested(st)) return;
+    const int n = *count;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            S.item = atomicAdd(next, 1);
+            S.nbig = 0;
+        }
+        __syncthreads();
+        const int d = S.item;
+        if (d >= n) break;
+        const Seg g = list[dir * d];
+        const double *in = (g.src ? tmp : keys) + g.start;
+        double *out = keys + g.start;
+        const int m = (int)g.len;
+        // 1. load (coalesced) + min / max
+        double mn = CUDART_INF, mx = -CUDART_INF;
+#pragma unroll 4
+        for (int i = tid; i < m; i += kT) {
+            const double x = in[i];
+            S.a[i] = x;
+            mn = x < mn ? x : mn;
+            mx = x > mx ? x : mx;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = p < mn ? p : mn;
+            mx = q > mx ? q : mx;
+        }
+        if (lane == 0) {
+            S.red[0][wid] = mn;
+            S.red[1][wid] = mx;
+        }
+        int B = m / kSortLambda;
+        B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
+        for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
+        __syncthreads();
+        mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
+        mx = lane < kWarps ? S.red[1][lane] : -CUDART_INF;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
+            mn = p < mn ? p : mn;
+            mx = q > mx ? q : mx;
+        }
+        const double lo = mn, hi = mx;
+        if (!(hi > lo)) {   // constant segment: already sorted
+            if (g.src)
+                for (int i = tid; i < m; i += kT) out[i] = S.a[i];
+        } else {
+            double scale = (double)B / (hi - lo);
+            if (!(scale > 0.0) || isinf(scale)) {   // range overflow / underflow: one bucket
+                B = 1;
+                scale = 0.0;
+            }
+            // 2. bucket histogram, scan, scatter a -> b
+#pragma unroll 4
+            for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[sort_bucket(S.a[i], lo, scale, B)], 1u);
+            __syncthreads();
+            {
+                const int b0 = tid * Smem::kPB;
+                unsigned c[Smem::kPB];
+                unsigned t = 0;
+#pragma unroll
+                for (int e = 0; e < Smem::kPB; ++e) {
+                    c[e] = b0 + e < B ? S.cur[b0 + e] : 0u;
+                    t += c[e];
+                }
+                unsigned ex = (unsigned)block_exclusive_scan((long long)t, S.sh, nullptr);
+#pragma unroll
+                for (int e = 0; e < Smem::kPB; ++e) {
+                    if (b0 + e < B) S.cur[b0 + e] = ex;
+                    ex += c[e];
+                }
+            }
+            __syncthreads();
+#pragma unroll 4
+            for (int i = tid; i < m; i += kT) {
+                const double x = S.a[i];
+                S.b[atomicAdd(&S.cur[sort_bucket(x, lo, scale, B)], 1u)] = x;
+            }
+            __syncthreads();
+            // 3. cur[b] is now the end of bucket b: small buckets by one thread each
+            for (int b = tid; b < B; b += kT) {
+                const int s0 = b ? (int)S.cur[b - 1] : 0;
+                const int sz = (int)S.cur[b] - s0;
+                if (sz <= 1) continue;
+                if (sz <= kThreadSortMax) {
+                    smem_insertion_sort(S.b + s0, sz);
+                } else {
+                    const int q = atomicAdd(&S.nbig, 1);
+                    S.big[q] = b;
+                }
+            }
+            __syncthreads();
+            // ... larger ones by one warp each
+            const int nbig = S.nbig;
+            for (int q = wid; q < nbig; q += kWarps) {
+                const int b = S.big[q];
+                const int s0 = b ? (int)S.cur[b - 1] : 0;
+                const int sz = (int)S.cur[b] - s0;
+                if (!warp_sort_bucket(S.b + s0, sz) && lane == 0) {   // skewed: back to the first-key partitioner
+                    const int li = atomicAdd(nlnext, 1);
+                    if (li < lcap) lnext[li] = make_seg(g.start + s0, sz, 0); else st->overflow = 6;
+                }
+            }
+            __syncthreads();
+            // 4. write back
+#pragma unroll 4
+            for (int i = tid; i < m; i += kT) out[i] = S.b[i];
+        }
+        if (tid == 0) {
+            add_bytes(st, kPhLeaf, 16ull * (unsigned long long)m);
+            atomicAdd(&st->keys_leaf, (unsigned long long)m);
+            atomicAdd(&st->leaves, 1ull);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host plumbing
 // ---------------------------------------------------------------------------
 static int sm_count()
@@ -996,6 +1234,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.n = n;
     L.seg_cap = (int)(n / (kLocalMax + 1) + 2);                  // global-pass segments
     L.lseg_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);          // local-partition segments per round
+    L.sseg_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);          // segment-sorter list (disjoint ranges)
     const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
@@ -1012,6 +1251,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.o_seg[1] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
     L.o_lseg[0] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
     L.o_lseg[1] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
+    L.o_sseg = off; off = align_up(off + sizeof(Seg) * L.sseg_cap);
     L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
     L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
     L.o_lut = off; off = align_up(off + sizeof(unsigned) * L.lut_cap);
@@ -1033,6 +1273,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     DevStatus *st = reinterpret_cast<DevStatus *>(w + L.o_status);
     Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.o_seg[0]), reinterpret_cast<Seg *>(w + L.o_seg[1])};
     Seg *lsegs[2] = {reinterpret_cast<Seg *>(w + L.o_lseg[0]), reinterpret_cast<Seg *>(w + L.o_lseg[1])};
+    Seg *ssegs = reinterpret_cast<Seg *>(w + L.o_sseg);
     int *chunk_seg = reinterpret_cast<int *>(w + L.o_chunk);
     double *piv = reinterpret_cast<double *>(w + L.o_piv);
     unsigned *lut = reinterpret_cast<unsigned *>(w + L.o_lut);
@@ -1044,6 +1285,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 
     KS_CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem)));
     KS_CK(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LocalSmem)));
+    KS_CK(cudaFuncSetAttribute(k_segsort<kSortThreads, kSortMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(SortSmem<kSortThreads, kSortMax>)));
+    KS_CK(cudaFuncSetAttribute(k_segsort<kSortSmallThreads, kSortBig>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(SortSmem<kSortSmallThreads, kSortBig>)));
     const int sms = sm_count();
     int occ_count = 1, occ_scatter = 1, occ_units = 1, occ_local = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_count, k_count<false>, kCountThreads, 0);
@@ -1054,6 +1299,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const int g_scatter = sms * (occ_scatter > 0 ? occ_scatter : 1);
     const int g_units = sms * (occ_units > 0 ? occ_units : 1);
     const int g_local = sms * (occ_local > 0 ? occ_local : 1);
+    int occ_sort_small = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sort_small, k_segsort<kSortSmallThreads, kSortBig>, kSortSmallThreads,
+                                                  sizeof(SortSmem<kSortSmallThreads, kSortBig>));
+    const int g_sort = sms;
+    const int g_sort_small = sms * (occ_sort_small > 0 ? occ_sort_small : 1);
     const int g_scan = sms * 2;
     const int g_seg = sms * 4;
     Launcher K(stream, profile);
@@ -1066,24 +1316,34 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         return h.overflow ? KS_CUDA_ERROR : KS_OK;
     };
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
+    int lc = 0;
     auto flush_units = [&]() {
+        // segment sorter first: its rare hand-backs go to the current local list
+        cudaMemsetAsync(&st->sort_next, 0, 2 * sizeof(int), stream);   // sort_next, sort_next_small
+        K.run(kPhLeaf, [&] {
+            k_segsort<kSortThreads, kSortMax><<<g_sort, kSortThreads, sizeof(SortSmem<kSortThreads, kSortMax>), stream>>>(
+                ssegs + (L.sseg_cap - 1), -1, &st->nsort_big, &st->sort_next, lsegs[lc], &st->nlocal[lc], L.lseg_cap,
+                st, keys, tmp);
+        });
+        K.run(kPhLeaf, [&] {
+            k_segsort<kSortSmallThreads, kSortBig><<<g_sort_small, kSortSmallThreads, sizeof(SortSmem<kSortSmallThreads, kSortBig>),
+                                           stream>>>(ssegs, 1, &st->nsort, &st->sort_next_small, lsegs[lc],
+                                                     &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+        });
+        cudaMemsetAsync(&st->nsort, 0, 2 * sizeof(int), stream);   // nsort, nsort_big
         K.run(kPhLeaf, [&] { k_finish_units<<<g_units, kUnitWarps * 32, 0, stream>>>(units, st, keys, tmp); });
         cudaMemsetAsync(&st->nunits, 0, sizeof(int), stream);
     };
 
     KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
     KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
+    const InitLists Lst{segs[0], lsegs[0], ssegs, units, L.seg_cap, L.lseg_cap, L.sseg_cap, L.unit_cap};
     if (d_off == nullptr) {
-        K.run(kPhGate, [&] {
-            k_init_single<<<1, 32, 0, stream>>>(n, segs[0], lsegs[0], units, st, L.seg_cap, L.lseg_cap, L.unit_cap);
-        });
+        K.run(kPhGate, [&] { k_init_single<<<1, 32, 0, stream>>>(n, Lst, st); });
         if (n <= kLocalMax)
             K.run(kPhGate, [&] { k_gate_segments<<<sms * 2, 256, 0, stream>>>(keys, nullptr, 0, n, st); });
     } else {
-        K.run(kPhGate, [&] {
-            k_init_segmented<<<sms, 256, 0, stream>>>(d_off, nseg0, segs[0], lsegs[0], units, st, L.seg_cap,
-                                                      L.lseg_cap, L.unit_cap);
-        });
+        K.run(kPhGate, [&] { k_init_segmented<<<sms, 256, 0, stream>>>(d_off, nseg0, Lst, st); });
         K.run(kPhGate, [&] { k_gate_segments<<<sms * 4, 256, 0, stream>>>(keys, d_off, nseg0, 0, st); });
     }
 
@@ -1092,7 +1352,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // at once when empty.  One status read at the end; inputs that need more
     // passes (adversarial shapes: presorted, few distinct values, ...) continue
     // in a synchronising loop.
-    int level = 0, gcur = 0, rounds = 0, lc = 0;
+    int level = 0, gcur = 0, rounds = 0;
     auto global_pass = [&]() {
         const double *src = (level & 1) ? tmp : keys;
         double *dst = (level & 1) ? keys : tmp;
@@ -1100,7 +1360,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         int *nseg_cur = &st->nseg[gcur];
         int *nseg_next = &st->nseg[gcur ^ 1];
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
-                   units, L.unit_cap, level};
+                   ssegs, &st->nsort, &st->nsort_big, L.sseg_cap, units, L.unit_cap, level};
         K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur); });
         K.run(kPhPivots, [&] {
             k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
@@ -1132,7 +1392,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream);
         cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
         EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
-                   L.lseg_cap, units, L.unit_cap, 128 + rounds};
+                   L.lseg_cap, ssegs, &st->nsort, &st->nsort_big, L.sseg_cap, units, L.unit_cap, 128 + rounds};
         K.run(kPhOther, [&] {
             k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
                                                                            L.lseg_cap, A, st, keys, tmp);
@@ -1151,7 +1411,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     int rc = sync_status();
     if (rc != KS_OK) return rc;
     // remaining work (rare): finish with host checks
-    while (!aborted() && (h.nseg[gcur] > 0 || h.nlocal[lc] + h.nlocal_big[lc] > 0 || h.nunits > 0)) {
+    while (!aborted() &&
+           (h.nseg[gcur] > 0 || h.nlocal[lc] + h.nlocal_big[lc] > 0 || h.nunits > 0 || h.nsort + h.nsort_big > 0)) {
         if (h.nseg[gcur] > 0) global_pass();
         else if (h.nlocal[lc] + h.nlocal_big[lc] > 0) local_round();
         if (h.nunits > L.unit_cap / 2 || (h.nseg[gcur] == 0 && h.nlocal[lc] + h.nlocal_big[lc] == 0)) flush_units();

@@ -24,15 +24,23 @@ constexpr int kPMax = 511;            // max pivot candidates (first P keys) per
 constexpr int kPMaxPow2 = 512;
 constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (1023)
 constexpr int kLutMax = 4096;         // LUT buckets (pow2 >= 8*P)
-constexpr int kKeysPerPivot = 64;     // P = len / 64 (capped): gaps average ~64..200 keys
+constexpr int kKeysPerPivot = 2048;   // P = len / 2048 (capped): gaps land in the segment sorter's range
 constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
 constexpr int kCountThreads = 512;
 constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
 constexpr int kPassThreads = 512;     // threads of scatter CTAs (8 keys each per tile)
 constexpr int kLocalMax = 49152;      // segments <= this are partitioned by one CTA (L2-resident)
-constexpr int kLocalBig = 12288;      // local segments above this are scheduled first (LPT)
+constexpr int kLocalBig = 32768;      // local segments above this are scheduled first (LPT)
 constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
-constexpr int kFillMin = 32;          // equality runs >= this are filled, not scattered
+constexpr int kFillMin = 1;           // equality runs >= this are filled, not scattered (all of them)
+// segment sorter: one CTA sorts a whole segment on chip (shared-memory copy ->
+// interpolation buckets -> per-thread / per-warp bucket sorts)
+constexpr int kSortThreads = 1024;
+constexpr int kSortMax = 12288;                       // keys (2 x 96 KB staging + buckets: one CTA per SM)
+constexpr int kSortSmallThreads = 256;                // CTA for segments <= kSortBig (3 CTAs per SM)
+constexpr int kSortBig = 4096;                        // larger segments go to the 1024-thread CTA
+constexpr int kSortLambda = 2;                        // mean keys per bucket
+constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
 constexpr int kLocalThreads = 512;    // CTA of the local partitioner
 constexpr int kUnitWarps = 8;         // warps per CTA of the unit sorter
 
@@ -54,6 +62,10 @@ struct DevStatus {
     int nlocal[2];                    // local-partition segments (current round, next round)
     int nlocal_big[2];                // ... of which > kLocalBig keys (stored from the top of the list)
     int local_next;                   // dynamic work counter of the local round
+    int nsort;                        // segment-sorter list (<= kSortBig keys, from index 0 upwards)
+    int nsort_big;                    // ... > kSortBig keys (stored from the top of the list)
+    int sort_next;                    // dynamic work counters of the segment sorter (big, small lists)
+    int sort_next_small;
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
