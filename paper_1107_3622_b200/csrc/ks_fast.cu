@@ -72,9 +72,9 @@ __device__ __forceinline__ Seg make_seg(long long start, long long len, int src)
 
 // Initial work lists (the first global / local round's tables).
 struct InitLists {
-    Seg *gsegs, *lsegs, *ssegs;
+    Seg *gsegs, *lsegs, *ssegs[kSortClasses];
     Item *units;
-    int seg_cap, lseg_cap, sseg_cap, unit_cap;
+    int seg_cap, lseg_cap, sseg_cap[kSortClasses], unit_cap;
 };
 
 // Route one segment at start: > kLocalMax keys -> global pass list,
@@ -91,12 +91,10 @@ __device__ __forceinline__ void route_initial(long long a, long long len, const 
     } else if (len > kSortMax) {
         int i = atomicAdd(&st->nlocal[0], 1);
         if (i < Lst.lseg_cap) Lst.lsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
-    } else if (len > kSortBig) {
-        int i = atomicAdd(&st->nsort_big, 1);
-        if (i < Lst.sseg_cap) Lst.ssegs[Lst.sseg_cap - 1 - i] = make_seg(a, len, 0); else st->overflow = 1;
     } else if (len > kUnitMax) {
-        int i = atomicAdd(&st->nsort, 1);
-        if (i < Lst.sseg_cap) Lst.ssegs[i] = make_seg(a, len, 0); else st->overflow = 1;
+        const int c = sort_class(len);
+        int i = atomicAdd(&st->nsort[c], 1);
+        if (i < Lst.sseg_cap[c]) Lst.ssegs[c][i] = make_seg(a, len, 0); else st->overflow = 1;
     } else if (len >= 2) {
         int i = atomicAdd(&st->nunits, 1);
         if (i < Lst.unit_cap) Lst.units[i] = make_item(a, len, kItemUnit, 0); else st->overflow = 1;
@@ -171,9 +169,10 @@ __global__ void k_gate_segments(const double *keys, const long long *off, long l
 // histogram of pivot buckets and an exclusive scan (a = #pivots in buckets
 // < t, b = #pivots in buckets <= t).
 // ---------------------------------------------------------------------------
+template <int N>
 struct PivotScratch {
-    double sp[kPMaxPow2];
-    double sq[kPMaxPow2];
+    double sp[N];
+    double sq[N];
     long long sh[33];
     int sk;
 };
@@ -193,7 +192,8 @@ __device__ __forceinline__ double merge_pick(const double *s, int g0, int size, 
     return (B[b] < A[a]) ? B[b] : A[a];
 }
 
-__device__ void build_pivots(const double *seg, int P, int Treq, double *piv, unsigned *lut, PivotScratch &W,
+template <int N>
+__device__ void build_pivots(const double *seg, int P, int Treq, double *piv, unsigned *lut, PivotScratch<N> &W,
                              int &k_out, int &T_out, double &lo_out, double &scale_out)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -285,18 +285,18 @@ __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, un
     scale_out = scale;
 }
 
-__host__ __device__ __forceinline__ int pivots_for(long long len)
+__host__ __device__ __forceinline__ int pivots_for(long long len, int pmax)
 {
     long long P = cdiv(len, kKeysPerPivot);
-    if (P > kPMax) P = kPMax;
+    if (P > pmax) P = pmax;
     if (P < 1) P = 1;
     return (int)P;
 }
 
-__host__ __device__ __forceinline__ int lut_for(int P)
+__host__ __device__ __forceinline__ int lut_for(int P, int tmax)
 {
     int T = P >= 2 ? next_pow2(8 * P) : 1;
-    return T > kLutMax ? kLutMax : T;
+    return T > tmax ? tmax : T;
 }
 
 // ---------------------------------------------------------------------------
@@ -307,10 +307,10 @@ __global__ void k_seg_prep(Seg *segs, const int *nseg)
     int ns = *nseg;
     for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
         Seg g = segs[s];
-        g.P = pivots_for(g.len);
+        g.P = pivots_for(g.len, kPMax);
         g.rows = 2 * g.P + 1;
         g.nch = (int)cdiv(g.len, kChunk);
-        g.T = lut_for(g.P);
+        g.T = lut_for(g.P, kLutMax);
         segs[s] = g;
     }
 }
@@ -357,12 +357,21 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
     }
 }
 
-__global__ void __launch_bounds__(256) k_pivots(Seg *segs, const int *nseg, const double *src, double *piv_pool,
-                                                unsigned *lut_pool, int *chunk_seg)
+struct PivotsSmem {
+    PivotScratch<kPMaxPow2> W;
+    double piv[kPMax + kPivPad];
+    unsigned lut[kLutMax];
+};
+constexpr int kPivotThreads = 1024;
+
+__global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *nseg, const double *src,
+                                                          double *piv_pool, unsigned *lut_pool, int *chunk_seg)
 {
-    __shared__ PivotScratch W;
-    __shared__ double piv[kPMax + kPivPad];
-    __shared__ unsigned lut[kLutMax];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    PivotsSmem &PS = *reinterpret_cast<PivotsSmem *>(smem_raw);
+    auto &W = PS.W;
+    double *piv = PS.piv;
+    unsigned *lut = PS.lut;
     const int ns = *nseg;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
         const Seg g = segs[s];
@@ -401,15 +410,23 @@ __device__ __forceinline__ void load_seg(const Seg *segs, int s, const double *p
     for (int i = threadIdx.x; i < sg.T; i += blockDim.x) P.lut[i] = lut_pool[sg.lut_off + i];
 }
 
+struct CountSmem {
+    PassSmem P;
+    unsigned hist[kRowsMax];
+    Seg sg;
+};
+
 template <bool kGate>
 __global__ void __launch_bounds__(kCountThreads) k_count(const Seg *segs, const int *chunk_seg, const DevStatus *cst,
                                                          const double *src, const double *piv_pool,
                                                          const unsigned *lut_pool, unsigned *mat, DevStatus *st)
 {
     constexpr int U = 8;   // keys in flight per lane
-    __shared__ PassSmem P;
-    __shared__ unsigned hist[kRowsMax];
-    __shared__ Seg sg;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CountSmem &CS = *reinterpret_cast<CountSmem *>(smem_raw);
+    PassSmem &P = CS.P;
+    unsigned *hist = CS.hist;
+    Seg &sg = CS.sg;
     int cached = -1;
     long long bad = LLONG_MAX;
     unsigned pz = 0, nz = 0;
@@ -520,17 +537,17 @@ __device__ __forceinline__ long long class_start(const Seg &g, const long long *
 
 // ---------------------------------------------------------------------------
 // scatter: classify again and send each key straight to its class slot:
-// slot = atomicAdd(cursor[class]) on a shared-memory cursor seeded with the
+// slot = atomicAdd(cursor[gap]) on a shared-memory cursor seeded with the
 // chunk's offset from the scanned count matrix (32-bit, relative to the
 // segment start).  No tile staging: on B200 the direct 8-byte scatter into
 // the L2-resident destination costs fewer shared-memory wavefronts than
 // staging runs (ncu: staged 1.56 wavefronts/key, smem-bound).  Equality
-// runs of at least kFillMin keys are not written: the finish pass fills them.
+// runs (odd classes) are not written: the finish pass fills them, so only
+// gap classes carry a cursor.
 // ---------------------------------------------------------------------------
 struct ScatterSmem {
     PassSmem P;
-    unsigned cursor[kRowsMax + 1];   // next slot per class, relative to the segment start
-    unsigned char skip[kRowsMax + 1];
+    unsigned cursor[kPMax + 1];   // next slot per gap class, relative to the segment start
     Seg sg;
 };
 
@@ -557,14 +574,10 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
         const long long base = g.start + (long long)j * kChunk;
         const int cnt = (int)min((long long)kChunk, g.len - (long long)j * kChunk);
         const long long base_i = moff[g.mat_off];
-        const int rows = g.rows, nch = g.nch, T = g.T;
+        const int nch = g.nch, T = g.T;
         const double lo = g.lo, scale = g.scale;
-        for (int c = threadIdx.x; c < rows; c += blockDim.x) {
-            const long long c0 = class_start(g, moff, base_i, c);
-            const long long tot = class_start(g, moff, base_i, c + 1) - c0;
-            S.skip[c] = ((c & 1) && tot >= kFillMin) ? 1 : 0;   // long equality run: filled by the finish pass
-            S.cursor[c] = (unsigned)(moff[g.mat_off + (long long)c * nch + j] - base_i);
-        }
+        for (int q = threadIdx.x; q <= g.k; q += blockDim.x)
+            S.cursor[q] = (unsigned)(moff[g.mat_off + (long long)(2 * q) * nch + j] - base_i);
         __syncthreads();
         const double *in = src + base + threadIdx.x;
         double *out = dst + g.start;
@@ -576,13 +589,13 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int c = classify(v[u], S.P.piv, S.P.lut, lo, scale, T);
-                if (!S.skip[c]) out[atomicAdd(&S.cursor[c], 1u)] = v[u];
+                if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u)] = v[u];
             }
         }
         for (int i = i0 + threadIdx.x; i < cnt; i += kPassThreads) {
             const double v = src[base + i];
             const int c = classify(v, S.P.piv, S.P.lut, lo, scale, T);
-            if (!S.skip[c]) out[atomicAdd(&S.cursor[c], 1u)] = v;
+            if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u)] = v;
         }
     }
 }
@@ -594,7 +607,7 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
 //  * gap <= kUnitMax (+ its short equality run)  -> one warp unit
 //  * kUnitMax < gap <= kLocalMax                 -> local-partition segment
 //  * gap > kLocalMax                             -> next global pass
-//  * equality run >= kFillMin                    -> fill (never scattered)
+//  * equality run (any length)                   -> fill (never scattered)
 // Lists are reserved per CTA with one atomic each.
 // ---------------------------------------------------------------------------
 struct EmitOut {
@@ -609,48 +622,51 @@ struct EmitArgs {
     int *nlnext;       // small local segments, stored from index 0 upwards
     int *nlnext_big;   // big local segments (> kLocalBig), stored from index lcap-1 downwards
     int lcap;
-    Seg *snext;        // segment-sorter list
-    int *nsnext;       // <= kSortBig keys, from index 0 upwards
-    int *nsnext_big;   // > kSortBig keys, from index scap-1 downwards
-    int scap;
+    Seg *snext[kSortClasses];   // segment-sorter lists by size class
+    int *nsnext;                // counters nsnext[0..kSortClasses)
+    int scap[kSortClasses];
     Item *units;
     int ucap;
     int tag_round;     // pass / round number: makes unit tags unique per partition
 };
 
 // packed per-thread list counts for one block scan: units (<= 2 per thread,
-// 11 bits) and five 0/1 list flags (10 bits each; blocks have <= 512 threads)
-constexpr int kPkU = 0, kPkS = 11, kPkSB = 21, kPkL = 31, kPkLB = 41, kPkG = 51;
+// 11 bits) and 0/1 list flags (10 bits each; blocks have <= 512 threads)
+constexpr int kPkU = 0, kPkL = 11, kPkLB = 21, kPkG = 31;
 __device__ __forceinline__ long long pk_get(long long x, int sh, int bits) { return (x >> sh) & ((1ll << bits) - 1); }
 
 __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
                               const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase, long long tag)
 {
     // every equality run (class 2j+1) is final: it is written as a fill of the pivot value
-    int u_gap = 0, s_gap = 0, sb_gap = 0, l_gap = 0, lb_gap = 0, g_gap = 0;
+    int u_gap = 0, s_cls = -1, l_gap = 0, lb_gap = 0, g_gap = 0;
     if (have && (gl >= 2 || (gl == 1 && dst_id == 1))) {
         if (gl <= kUnitMax) u_gap = 1;
-        else if (gl <= kSortBig) s_gap = 1;
-        else if (gl <= kSortMax) sb_gap = 1;
+        else if (gl <= kSortMax) s_cls = sort_class(gl);
         else if (gl <= kLocalBig) l_gap = 1;
         else if (gl <= kLocalMax) lb_gap = 1;
         else g_gap = 1;
     }
     const int f_eq = (have && el > 0) ? 1 : 0;
     const int nu = u_gap + f_eq;
-    const long long pk = ((long long)nu << kPkU) | ((long long)s_gap << kPkS) | ((long long)sb_gap << kPkSB) |
-                         ((long long)l_gap << kPkL) | ((long long)lb_gap << kPkLB) | ((long long)g_gap << kPkG);
-    long long tpk;
+    const long long pk = ((long long)nu << kPkU) | ((long long)l_gap << kPkL) | ((long long)lb_gap << kPkLB) |
+                         ((long long)g_gap << kPkG);
+    const long long pks = s_cls < 0 ? 0ll : (1ll << (20 * s_cls));   // sort classes: 20 bits each
+    long long tpk, tpks;
     const long long xpk = block_exclusive_scan(pk, sh, &tpk);
+    const long long xpks = block_exclusive_scan(pks, sh, &tpks);
     if (threadIdx.x == 0) {
-        const int tu = (int)pk_get(tpk, kPkU, 11), ts = (int)pk_get(tpk, kPkS, 10), tsb = (int)pk_get(tpk, kPkSB, 10);
-        const int tl = (int)pk_get(tpk, kPkL, 10), tlb = (int)pk_get(tpk, kPkLB, 10), tg = (int)pk_get(tpk, kPkG, 10);
+        const int tu = (int)pk_get(tpk, kPkU, 11), tl = (int)pk_get(tpk, kPkL, 10);
+        const int tlb = (int)pk_get(tpk, kPkLB, 10), tg = (int)pk_get(tpk, kPkG, 10);
         sbase[0] = tu ? atomicAdd(&st->nunits, tu) : 0;
         sbase[1] = tl ? atomicAdd(A.nlnext, tl) : 0;
         sbase[2] = tg ? atomicAdd(A.ngnext, tg) : 0;
         sbase[3] = tlb ? atomicAdd(A.nlnext_big, tlb) : 0;
-        sbase[4] = ts ? atomicAdd(A.nsnext, ts) : 0;
-        sbase[5] = tsb ? atomicAdd(A.nsnext_big, tsb) : 0;
+#pragma unroll
+        for (int c = 0; c < kSortClasses; ++c) {
+            const int ts = (int)pk_get(tpks, 20 * c, 20);
+            sbase[4 + c] = ts ? atomicAdd(&A.nsnext[c], ts) : 0;
+        }
     }
     __syncthreads();
     long long ui = sbase[0] + pk_get(xpk, kPkU, 11);
@@ -663,13 +679,9 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         it.value = pv;
         if (ui < A.ucap) A.units[ui] = it; else st->overflow = 3;
     }
-    if (s_gap) {
-        const long long i = sbase[4] + pk_get(xpk, kPkS, 10);
-        if (i < A.scap) A.snext[i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
-    }
-    if (sb_gap) {
-        const long long i = A.scap - 1 - (sbase[5] + pk_get(xpk, kPkSB, 10));
-        if (i >= 0) A.snext[i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
+    if (s_cls >= 0) {
+        const long long i = sbase[4 + s_cls] + pk_get(xpks, 20 * s_cls, 20);
+        if (i < A.scap[s_cls]) A.snext[s_cls][i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
     }
     if (l_gap) {
         const long long li = sbase[1] + pk_get(xpk, kPkL, 10);
@@ -709,35 +721,41 @@ __device__ __forceinline__ void account_partition(DevStatus *st, long long len, 
 // plan (global pass): class extents from the scanned count matrix
 // ---------------------------------------------------------------------------
 constexpr int kPlanThreads = 512;
-static_assert(kPMax + 1 <= kPlanThreads, "one pivot pair per thread");
 
 __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const int *nseg, const double *piv_pool,
                                                        const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
 {
     __shared__ long long sh[33];
-    __shared__ long long sbase[6];
+    __shared__ long long sbase[4 + kSortClasses];
     if (abort_requested(st)) return;
     const int ns = *nseg;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
         __syncthreads();
         const Seg g = segs[s];
         const long long base_i = moff[g.mat_off];
-        const int j = threadIdx.x;
-        const bool have = j <= g.k;
-        long long ag = 0, gl = 0, ae = 0, el = 0;
-        double pv = 0.0;
-        if (have) {
-            ag = class_start(g, moff, base_i, 2 * j);
-            ae = class_start(g, moff, base_i, 2 * j + 1);
-            gl = ae - ag;
-            if (j < g.k) {
-                el = class_start(g, moff, base_i, 2 * j + 2) - ae;
-                pv = piv_pool[g.piv_off + j];
+        EmitOut tot{0, 0, 0};
+        // pivot pairs (gap 2j, run 2j+1), kPlanThreads at a time
+        for (int j0 = 0; j0 <= g.k; j0 += kPlanThreads) {
+            const int j = j0 + threadIdx.x;
+            const bool have = j <= g.k;
+            long long ag = 0, gl = 0, ae = 0, el = 0;
+            double pv = 0.0;
+            if (have) {
+                ag = class_start(g, moff, base_i, 2 * j);
+                ae = class_start(g, moff, base_i, 2 * j + 1);
+                gl = ae - ag;
+                if (j < g.k) {
+                    el = class_start(g, moff, base_i, 2 * j + 2) - ae;
+                    pv = piv_pool[g.piv_off + j];
+                }
             }
+            const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase,
+                                         (g.start << 8) | (A.tag_round & 0xff));
+            tot.unit_keys += o.unit_keys;
+            tot.fill_keys += o.fill_keys;
+            tot.items += o.items;
         }
-        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase,
-                                     (g.start << 8) | (A.tag_round & 0xff));
-        if (threadIdx.x == 0) account_partition(st, g.len, o, false);
+        if (threadIdx.x == 0) account_partition(st, g.len, tot, false);
     }
 }
 
@@ -749,13 +767,13 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
 // a device work counter.
 // ---------------------------------------------------------------------------
 struct LocalSmem {
-    PivotScratch W;
-    double piv[kPMax + kPivPad];
-    unsigned lut[kLutMax];
-    unsigned hist[kRowsMax + 1];
-    unsigned cursor[kRowsMax + 1];
+    PivotScratch<kPMaxLocal + 1> W;
+    double piv[kPMaxLocal + kPivPad];
+    unsigned lut[kLutMaxLocal];
+    unsigned hist[kRowsMaxLocal + 1];
+    unsigned cursor[kRowsMaxLocal + 1];
     long long sh[33];
-    long long sbase[6];
+    long long sbase[4 + kSortClasses];
     int item;
 };
 
@@ -779,11 +797,11 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
         double *dst = (g.src ? keys : tmp) + g.start;
         const int dst_id = g.src ? 0 : 1;
         const int m = (int)g.len;
-        const int P = pivots_for(m);
+        const int P = pivots_for(m, kPMaxLocal);
         int k, T;
         double lo, scale;
         KS_TR_DECL;
-        build_pivots(src, P, lut_for(P), L.piv, L.lut, L.W, k, T, lo, scale);
+        build_pivots(src, P, lut_for(P, kLutMaxLocal), L.piv, L.lut, L.W, k, T, lo, scale);
         KS_TR(0);
         const int rows = 2 * k + 1;
         for (int c = threadIdx.x; c < rows; c += blockDim.x) L.hist[c] = 0;
@@ -818,13 +836,13 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int c = classify(v[u], L.piv, L.lut, lo, scale, T);
-                if (!(c & 1) || L.hist[c] < (unsigned)kFillMin) dst[atomicAdd(&L.cursor[c], 1u)] = v[u];
+                if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v[u];
             }
         }
         for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads) {
             const double v = src[i];
             const int c = classify(v, L.piv, L.lut, lo, scale, T);
-            if (!(c & 1) || L.hist[c] < (unsigned)kFillMin) dst[atomicAdd(&L.cursor[c], 1u)] = v;
+            if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v;
         }
         __syncthreads();
         KS_TR(2);
@@ -838,7 +856,7 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
             ag = (long long)L.cursor[2 * j] - gl;
             if (j < k) {
                 el = L.hist[2 * j + 1];
-                ae = (long long)L.cursor[2 * j + 1] - (el < kFillMin ? el : 0);
+                ae = (long long)L.cursor[2 * j + 1];   // equality runs are not scattered: cursor = start
                 pv = L.piv[j];
             }
         }
@@ -949,13 +967,14 @@ struct SortSmem {
     static constexpr int kPB = kBuckets / kT;               // buckets per thread in the scan
     static constexpr int kBigCap = kCap / (kThreadSortMax + 1) + 1;
     double a[kCap];        // the segment as loaded
-    double b[kCap];        // bucket order, sorted in place
+    double b[kCap];        // bucket order
     unsigned cur[kBuckets];
     int big[kBigCap];
     double red[2][32];
-    long long sh[33];
-    int nbig;
-    int item;
+    double bounds[2];      // lo, scale
+    unsigned sh[33];
+    long long start;       // descriptor of the segment being processed (prefetched by thread 0)
+    int len, src, item, nbig;
 };
 
 __device__ __forceinline__ int sort_bucket(double v, double lo, double scale, int B)
@@ -1016,12 +1035,14 @@ __device__ __noinline__ bool warp_sort_bucket(double *a, int sz)
     return true;
 }
 
-// One list of the segment sorter: entries list[dir * d] for d < *count
-// (dir = -1 walks the big-segment half from the top of the array).
+// One size class of the segment sorter: entries list[d] for d < *count,
+// pulled from a work counter; thread 0 prefetches the next descriptor while
+// the block works on the current one.  The per-segment code path is kept
+// short (no unrolled remainders): segments hold only ~10 keys per thread.
 template <int kT, int kCap>
-__global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : 3)
-    k_segsort(const Seg *list, int dir, const int *count, int *next, Seg *lnext, int *nlnext, int lcap,
-              DevStatus *st, double *keys, const double *tmp)
+__global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 5))
+    k_segsort(const Seg *list, const int *count, int *next, Seg *lnext, int *nlnext, int lcap, DevStatus *st,
+              double *keys, const double *tmp)
 {
     using Smem = SortSmem<kT, kCap>;
     constexpr int kWarps = kT / 32;
@@ -1031,27 +1052,57 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : 3)
     if (abort_requested(st)) return;
     const int n = *count;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    for (;;) {
-        __syncthreads();
-        if (tid == 0) {
-            S.item = atomicAdd(next, 1);
-            S.nbig = 0;
+    if (tid == 0) {
+        const int d = atomicAdd(next, 1);
+        S.item = d;
+        S.nbig = 0;
+        if (d < n) {
+            const Seg g = list[d];
+            S.start = g.start;
+            S.len = (int)g.len;
+            S.src = g.src;
         }
-        __syncthreads();
-        const int d = S.item;
-        if (d >= n) break;
-        const Seg g = list[dir * d];
-        const double *in = (g.src ? tmp : keys) + g.start;
-        double *out = keys + g.start;
-        const int m = (int)g.len;
-        // 1. load (coalesced) + min / max
+    }
+    __syncthreads();
+    unsigned long long keys_done = 0, segs_done = 0;
+    for (;;) {
+        if (S.item >= n) break;
+        const long long start = S.start;
+        const int m = S.len;
+        const double *in = (S.src ? tmp : keys) + start;
+        double *out = keys + start;
+        const bool copy_const = S.src != 0;
+        // thread 0: claim and load the next descriptor (lands in smem at the end)
+        int nd = 0;
+        long long nstart = 0;
+        int nlen = 0, nsrc = 0;
+        if (tid == 0) {
+            nd = atomicAdd(next, 1);
+            if (nd < n) {
+                const Seg g = list[nd];
+                nstart = g.start;
+                nlen = (int)g.len;
+                nsrc = g.src;
+            }
+        }
+        // 1. load (coalesced, 4 loads in flight per thread) + min / max
         double mn = CUDART_INF, mx = -CUDART_INF;
-#pragma unroll 4
-        for (int i = tid; i < m; i += kT) {
-            const double x = in[i];
-            S.a[i] = x;
-            mn = x < mn ? x : mn;
-            mx = x > mx ? x : mx;
+        for (int i0 = 0; i0 < m; i0 += 4 * kT) {
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kT + tid;
+                x[u] = i < m ? in[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + u * kT + tid;
+                if (i < m) {
+                    S.a[i] = x[u];
+                    mn = x[u] < mn ? x[u] : mn;
+                    mx = x[u] > mx ? x[u] : mx;
+                }
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -1065,28 +1116,37 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : 3)
         }
         int B = m / kSortLambda;
         B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
+#pragma unroll 1
         for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
         __syncthreads();
-        mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
-        mx = lane < kWarps ? S.red[1][lane] : -CUDART_INF;
+        if (wid == 0) {   // block min / max and the bucket scale, broadcast through shared memory
+            mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
+            mx = lane < kWarps ? S.red[1][lane] : -CUDART_INF;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
-            mn = p < mn ? p : mn;
-            mx = q > mx ? q : mx;
-        }
-        const double lo = mn, hi = mx;
-        if (!(hi > lo)) {   // constant segment: already sorted
-            if (g.src)
-                for (int i = tid; i < m; i += kT) out[i] = S.a[i];
-        } else {
-            double scale = (double)B / (hi - lo);
-            if (!(scale > 0.0) || isinf(scale)) {   // range overflow / underflow: one bucket
-                B = 1;
-                scale = 0.0;
+            for (int o = 16; o > 0; o >>= 1) {
+                const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
+                mn = p < mn ? p : mn;
+                mx = q > mx ? q : mx;
             }
+            if (lane == 0) {
+                double scale = mx > mn ? (double)B / (mx - mn) : -1.0;            // -1: constant segment
+                if (mx > mn && (!(scale > 0.0) || isinf(scale))) scale = 0.0;    // range overflow / underflow
+                S.bounds[0] = mn;
+                S.bounds[1] = scale;
+            }
+        }
+        __syncthreads();
+        const double lo = S.bounds[0];
+        const double scale = S.bounds[1];
+        if (scale < 0.0) {   // constant segment: already sorted
+            if (copy_const) {
+#pragma unroll 1
+                for (int i = tid; i < m; i += kT) out[i] = S.a[i];
+            }
+        } else {
+            if (scale == 0.0) B = 1;   // one bucket: the warp path (or the partitioner) takes it
             // 2. bucket histogram, scan, scatter a -> b
-#pragma unroll 4
+#pragma unroll 1
             for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[sort_bucket(S.a[i], lo, scale, B)], 1u);
             __syncthreads();
             {
@@ -1098,54 +1158,80 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : 3)
                     c[e] = b0 + e < B ? S.cur[b0 + e] : 0u;
                     t += c[e];
                 }
-                unsigned ex = (unsigned)block_exclusive_scan((long long)t, S.sh, nullptr);
+                unsigned ex = block_exclusive_scan_u32(t, S.sh, nullptr);
+                unsigned bigmask = 0;
 #pragma unroll
                 for (int e = 0; e < Smem::kPB; ++e) {
                     if (b0 + e < B) S.cur[b0 + e] = ex;
                     ex += c[e];
+                    bigmask |= (c[e] > (unsigned)kThreadSortMax ? 1u : 0u) << e;
+                }
+                while (bigmask) {   // rare: buckets for the warp path
+                    const int e = __ffs(bigmask) - 1;
+                    bigmask &= bigmask - 1;
+                    S.big[atomicAdd(&S.nbig, 1)] = b0 + e;
                 }
             }
             __syncthreads();
-#pragma unroll 4
+#pragma unroll 1
             for (int i = tid; i < m; i += kT) {
                 const double x = S.a[i];
                 S.b[atomicAdd(&S.cur[sort_bucket(x, lo, scale, B)], 1u)] = x;
             }
             __syncthreads();
-            // 3. cur[b] is now the end of bucket b: small buckets by one thread each
-            for (int b = tid; b < B; b += kT) {
-                const int s0 = b ? (int)S.cur[b - 1] : 0;
-                const int sz = (int)S.cur[b] - s0;
-                if (sz <= 1) continue;
-                if (sz <= kThreadSortMax) {
-                    smem_insertion_sort(S.b + s0, sz);
-                } else {
-                    const int q = atomicAdd(&S.nbig, 1);
-                    S.big[q] = b;
-                }
-            }
-            __syncthreads();
-            // ... larger ones by one warp each
+            // 3. cur[b] is now the end of bucket b.  Buckets of more than
+            //    kThreadSortMax keys (listed by the scan; none for smooth
+            //    inputs) are sorted in place by one warp each.
             const int nbig = S.nbig;
-            for (int q = wid; q < nbig; q += kWarps) {
-                const int b = S.big[q];
-                const int s0 = b ? (int)S.cur[b - 1] : 0;
-                const int sz = (int)S.cur[b] - s0;
-                if (!warp_sort_bucket(S.b + s0, sz) && lane == 0) {   // skewed: back to the first-key partitioner
-                    const int li = atomicAdd(nlnext, 1);
-                    if (li < lcap) lnext[li] = make_seg(g.start + s0, sz, 0); else st->overflow = 6;
+            if (nbig) {
+                for (int q = wid; q < nbig; q += kWarps) {
+                    const int b = S.big[q];
+                    const int s0 = b ? (int)S.cur[b - 1] : 0;
+                    const int sz = (int)S.cur[b] - s0;
+                    if (!warp_sort_bucket(S.b + s0, sz) && lane == 0) {   // skewed: back to the first-key partitioner
+                        const int li = atomicAdd(nlnext, 1);
+                        if (li < lcap) lnext[li] = make_seg(start + s0, sz, 0); else st->overflow = 6;
+                    }
                 }
+                __syncthreads();
             }
-            __syncthreads();
-            // 4. write back
-#pragma unroll 4
-            for (int i = tid; i < m; i += kT) out[i] = S.b[i];
+            // 4. every key of a small bucket takes its rank inside the bucket
+            //    (ties by position: equal keys are bitwise equal here) and is
+            //    written straight to its final place
+#pragma unroll 1
+            for (int i = tid; i < m; i += kT) {
+                const double x = S.b[i];
+                const int bk = sort_bucket(x, lo, scale, B);
+                const int e = (int)S.cur[bk];
+                const int s0 = bk ? (int)S.cur[bk - 1] : 0;
+                int pos = i;
+                if (e - s0 > 1 && e - s0 <= kThreadSortMax) {
+                    int r = s0;
+#pragma unroll 1
+                    for (int j = s0; j < e; ++j) {
+                        const double y = S.b[j];
+                        r += (y < x || (y == x && j < i)) ? 1 : 0;
+                    }
+                    pos = r;
+                }
+                out[pos] = x;
+            }
         }
+        keys_done += (unsigned long long)m;
+        segs_done += 1;
         if (tid == 0) {
-            add_bytes(st, kPhLeaf, 16ull * (unsigned long long)m);
-            atomicAdd(&st->keys_leaf, (unsigned long long)m);
-            atomicAdd(&st->leaves, 1ull);
+            S.item = nd;
+            S.start = nstart;
+            S.len = nlen;
+            S.src = nsrc;
+            S.nbig = 0;
         }
+        __syncthreads();
+    }
+    if (tid == 0 && segs_done) {
+        add_bytes(st, kPhLeaf, 16ull * keys_done);
+        atomicAdd(&st->keys_leaf, keys_done);
+        atomicAdd(&st->leaves, segs_done);
     }
 }
 
@@ -1234,7 +1320,8 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.n = n;
     L.seg_cap = (int)(n / (kLocalMax + 1) + 2);                  // global-pass segments
     L.lseg_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);          // local-partition segments per round
-    L.sseg_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);          // segment-sorter list (disjoint ranges)
+    for (int c = 0; c < kSortClasses; ++c)                       // segment-sorter lists (disjoint ranges)
+        L.sseg_cap[c] = (int)(n / ((c ? sort_cap(c - 1) : kUnitMax) + 1) + nseg0 + 2);
     const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
@@ -1251,7 +1338,10 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.o_seg[1] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
     L.o_lseg[0] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
     L.o_lseg[1] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
-    L.o_sseg = off; off = align_up(off + sizeof(Seg) * L.sseg_cap);
+    for (int c = 0; c < kSortClasses; ++c) {
+        L.o_sseg[c] = off;
+        off = align_up(off + sizeof(Seg) * L.sseg_cap[c]);
+    }
     L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
     L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
     L.o_lut = off; off = align_up(off + sizeof(unsigned) * L.lut_cap);
@@ -1273,7 +1363,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     DevStatus *st = reinterpret_cast<DevStatus *>(w + L.o_status);
     Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.o_seg[0]), reinterpret_cast<Seg *>(w + L.o_seg[1])};
     Seg *lsegs[2] = {reinterpret_cast<Seg *>(w + L.o_lseg[0]), reinterpret_cast<Seg *>(w + L.o_lseg[1])};
-    Seg *ssegs = reinterpret_cast<Seg *>(w + L.o_sseg);
+    Seg *ssegs[kSortClasses];
+    for (int c = 0; c < kSortClasses; ++c) ssegs[c] = reinterpret_cast<Seg *>(w + L.o_sseg[c]);
     int *chunk_seg = reinterpret_cast<int *>(w + L.o_chunk);
     double *piv = reinterpret_cast<double *>(w + L.o_piv);
     unsigned *lut = reinterpret_cast<unsigned *>(w + L.o_lut);
@@ -1285,13 +1376,18 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 
     KS_CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem)));
     KS_CK(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LocalSmem)));
-    KS_CK(cudaFuncSetAttribute(k_segsort<kSortThreads, kSortMax>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(SortSmem<kSortThreads, kSortMax>)));
-    KS_CK(cudaFuncSetAttribute(k_segsort<kSortSmallThreads, kSortBig>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(SortSmem<kSortSmallThreads, kSortBig>)));
+    KS_CK(cudaFuncSetAttribute(k_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PivotsSmem)));
+    KS_CK(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
+    KS_CK(cudaFuncSetAttribute(k_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
+    KS_CK(cudaFuncSetAttribute(k_segsort<sort_threads(0), sort_cap(0)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(SortSmem<sort_threads(0), sort_cap(0)>)));
+    KS_CK(cudaFuncSetAttribute(k_segsort<sort_threads(1), sort_cap(1)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(SortSmem<sort_threads(1), sort_cap(1)>)));
+    KS_CK(cudaFuncSetAttribute(k_segsort<sort_threads(2), sort_cap(2)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)sizeof(SortSmem<sort_threads(2), sort_cap(2)>)));
     const int sms = sm_count();
     int occ_count = 1, occ_scatter = 1, occ_units = 1, occ_local = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_count, k_count<false>, kCountThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_count, k_count<false>, kCountThreads, sizeof(CountSmem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_scatter, k_scatter, kPassThreads, sizeof(ScatterSmem));
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_units, k_finish_units, kUnitWarps * 32, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_local, k_local, kLocalThreads, sizeof(LocalSmem));
@@ -1299,13 +1395,22 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const int g_scatter = sms * (occ_scatter > 0 ? occ_scatter : 1);
     const int g_units = sms * (occ_units > 0 ? occ_units : 1);
     const int g_local = sms * (occ_local > 0 ? occ_local : 1);
-    int occ_sort_small = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_sort_small, k_segsort<kSortSmallThreads, kSortBig>, kSortSmallThreads,
-                                                  sizeof(SortSmem<kSortSmallThreads, kSortBig>));
-    const int g_sort = sms;
-    const int g_sort_small = sms * (occ_sort_small > 0 ? occ_sort_small : 1);
+    int g_sortc[kSortClasses];
+    {
+        int o0 = 1, o1 = 1, o2 = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, k_segsort<sort_threads(0), sort_cap(0)>, sort_threads(0),
+                                                      sizeof(SortSmem<sort_threads(0), sort_cap(0)>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_segsort<sort_threads(1), sort_cap(1)>, sort_threads(1),
+                                                      sizeof(SortSmem<sort_threads(1), sort_cap(1)>));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_segsort<sort_threads(2), sort_cap(2)>, sort_threads(2),
+                                                      sizeof(SortSmem<sort_threads(2), sort_cap(2)>));
+        g_sortc[0] = sms * (o0 > 0 ? o0 : 1);
+        g_sortc[1] = sms * (o1 > 0 ? o1 : 1);
+        g_sortc[2] = sms * (o2 > 0 ? o2 : 1);
+    }
     const int g_scan = sms * 2;
     const int g_seg = sms * 4;
+    const int g_pivots = sms;
     Launcher K(stream, profile);
 
     DevStatus h{};
@@ -1319,25 +1424,32 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     int lc = 0;
     auto flush_units = [&]() {
         // segment sorter first: its rare hand-backs go to the current local list
-        cudaMemsetAsync(&st->sort_next, 0, 2 * sizeof(int), stream);   // sort_next, sort_next_small
+        cudaMemsetAsync(st->sort_next, 0, sizeof(st->sort_next), stream);
+        // largest class first: its CTAs hold a whole SM each
         K.run(kPhLeaf, [&] {
-            k_segsort<kSortThreads, kSortMax><<<g_sort, kSortThreads, sizeof(SortSmem<kSortThreads, kSortMax>), stream>>>(
-                ssegs + (L.sseg_cap - 1), -1, &st->nsort_big, &st->sort_next, lsegs[lc], &st->nlocal[lc], L.lseg_cap,
-                st, keys, tmp);
+            k_segsort<sort_threads(2), sort_cap(2)><<<g_sortc[2], sort_threads(2), sizeof(SortSmem<sort_threads(2), sort_cap(2)>),
+                                                      stream>>>(ssegs[2], &st->nsort[2], &st->sort_next[2], lsegs[lc],
+                                                                &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] {
-            k_segsort<kSortSmallThreads, kSortBig><<<g_sort_small, kSortSmallThreads, sizeof(SortSmem<kSortSmallThreads, kSortBig>),
-                                           stream>>>(ssegs, 1, &st->nsort, &st->sort_next_small, lsegs[lc],
-                                                     &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            k_segsort<sort_threads(1), sort_cap(1)><<<g_sortc[1], sort_threads(1), sizeof(SortSmem<sort_threads(1), sort_cap(1)>),
+                                                      stream>>>(ssegs[1], &st->nsort[1], &st->sort_next[1], lsegs[lc],
+                                                                &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
-        cudaMemsetAsync(&st->nsort, 0, 2 * sizeof(int), stream);   // nsort, nsort_big
+        K.run(kPhLeaf, [&] {
+            k_segsort<sort_threads(0), sort_cap(0)><<<g_sortc[0], sort_threads(0), sizeof(SortSmem<sort_threads(0), sort_cap(0)>),
+                                                      stream>>>(ssegs[0], &st->nsort[0], &st->sort_next[0], lsegs[lc],
+                                                                &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+        });
+        cudaMemsetAsync(st->nsort, 0, sizeof(st->nsort), stream);
         K.run(kPhLeaf, [&] { k_finish_units<<<g_units, kUnitWarps * 32, 0, stream>>>(units, st, keys, tmp); });
         cudaMemsetAsync(&st->nunits, 0, sizeof(int), stream);
     };
 
     KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
     KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
-    const InitLists Lst{segs[0], lsegs[0], ssegs, units, L.seg_cap, L.lseg_cap, L.sseg_cap, L.unit_cap};
+    const InitLists Lst{segs[0], lsegs[0], {ssegs[0], ssegs[1], ssegs[2]}, units, L.seg_cap, L.lseg_cap,
+                        {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]}, L.unit_cap};
     if (d_off == nullptr) {
         K.run(kPhGate, [&] { k_init_single<<<1, 32, 0, stream>>>(n, Lst, st); });
         if (n <= kLocalMax)
@@ -1360,19 +1472,22 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         int *nseg_cur = &st->nseg[gcur];
         int *nseg_next = &st->nseg[gcur ^ 1];
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
-                   ssegs, &st->nsort, &st->nsort_big, L.sseg_cap, units, L.unit_cap, level};
+                   {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
+                   units, L.unit_cap, level};
         K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur); });
         K.run(kPhPivots, [&] {
             k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
         });
-        K.run(kPhPivots, [&] { k_pivots<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg); });
+        K.run(kPhPivots, [&] {
+            k_pivots<<<g_pivots, kPivotThreads, sizeof(PivotsSmem), stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
+        });
         if (level == 0)
             K.run(kPhCount, [&] {
-                k_count<true><<<g_count, kCountThreads, 0, stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
+                k_count<true><<<g_count, kCountThreads, sizeof(CountSmem), stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
         else
             K.run(kPhCount, [&] {
-                k_count<false><<<g_count, kCountThreads, 0, stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
+                k_count<false><<<g_count, kCountThreads, sizeof(CountSmem), stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
         K.run(kPhScan, [&] { k_scan_reduce<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum); });
         K.run(kPhScan, [&] { k_scan_bsums<<<1, 1024, 0, stream>>>(bsum, st); });
@@ -1392,7 +1507,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream);
         cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
         EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
-                   L.lseg_cap, ssegs, &st->nsort, &st->nsort_big, L.sseg_cap, units, L.unit_cap, 128 + rounds};
+                   L.lseg_cap, {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
+                   units, L.unit_cap, 128 + rounds};
         K.run(kPhOther, [&] {
             k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
                                                                            L.lseg_cap, A, st, keys, tmp);
@@ -1403,7 +1519,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         ++rounds;
     };
     // speculative part: expected shape of a random input
-    const int spec_global = n > kLocalMax ? (n > 4 * 1048576 ? 2 : 1) : 0;
+    const int spec_global = n > kLocalMax ? 1 : 0;
     for (int i = 0; i < spec_global; ++i) global_pass();
     local_round();
     local_round();
@@ -1412,7 +1528,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     if (rc != KS_OK) return rc;
     // remaining work (rare): finish with host checks
     while (!aborted() &&
-           (h.nseg[gcur] > 0 || h.nlocal[lc] + h.nlocal_big[lc] > 0 || h.nunits > 0 || h.nsort + h.nsort_big > 0)) {
+           (h.nseg[gcur] > 0 || h.nlocal[lc] + h.nlocal_big[lc] > 0 || h.nunits > 0 ||
+            h.nsort[0] + h.nsort[1] + h.nsort[2] > 0)) {
         if (h.nseg[gcur] > 0) global_pass();
         else if (h.nlocal[lc] + h.nlocal_big[lc] > 0) local_round();
         if (h.nunits > L.unit_cap / 2 || (h.nseg[gcur] == 0 && h.nlocal[lc] + h.nlocal_big[lc] == 0)) flush_units();

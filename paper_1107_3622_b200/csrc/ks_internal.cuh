@@ -20,25 +20,30 @@ namespace ks {
 // ---------------------------------------------------------------------------
 // Fast-mode tunables.
 // ---------------------------------------------------------------------------
-constexpr int kPMax = 511;            // max pivot candidates (first P keys) per global pass
-constexpr int kPMaxPow2 = 512;
-constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (1023)
-constexpr int kLutMax = 4096;         // LUT buckets (pow2 >= 8*P)
+constexpr int kPMax = 2047;           // max pivot candidates (first P keys) per global pass
+constexpr int kPMaxPow2 = 2048;
+constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (4095)
+constexpr int kLutMax = 8192;         // LUT buckets (pow2 >= 4*P)
+constexpr int kPMaxLocal = 255;       // ... per local partition (P = len / kKeysPerPivot <= 64)
+constexpr int kRowsMaxLocal = 2 * kPMaxLocal + 1;
+constexpr int kLutMaxLocal = 2048;
 constexpr int kKeysPerPivot = 2048;   // P = len / 2048 (capped): gaps land in the segment sorter's range
 constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
 constexpr int kCountThreads = 512;
 constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
 constexpr int kPassThreads = 512;     // threads of scatter CTAs (8 keys each per tile)
-constexpr int kLocalMax = 49152;      // segments <= this are partitioned by one CTA (L2-resident)
+constexpr int kLocalMax = 131072;     // segments <= this are partitioned by one CTA (L2-resident)
 constexpr int kLocalBig = 32768;      // local segments above this are scheduled first (LPT)
 constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
-constexpr int kFillMin = 1;           // equality runs >= this are filled, not scattered (all of them)
 // segment sorter: one CTA sorts a whole segment on chip (shared-memory copy ->
-// interpolation buckets -> per-thread / per-warp bucket sorts)
-constexpr int kSortThreads = 1024;
-constexpr int kSortMax = 12288;                       // keys (2 x 96 KB staging + buckets: one CTA per SM)
-constexpr int kSortSmallThreads = 256;                // CTA for segments <= kSortBig (3 CTAs per SM)
-constexpr int kSortBig = 4096;                        // larger segments go to the 1024-thread CTA
+// interpolation buckets -> per-thread / per-warp bucket sorts).  Three size
+// classes, each with its own CTA shape so that every thread holds 12..16 keys:
+//   class 0: <= 2048 keys, 128 threads;  class 1: <= 6144, 512;  class 2: <= 12288, 1024
+constexpr int kSortClasses = 3;
+constexpr int kSortMax = 12288;
+__host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? 2048 : (c == 1 ? 6144 : kSortMax); }
+__host__ __device__ constexpr int sort_threads(int c) { return c == 0 ? 128 : (c == 1 ? 512 : 1024); }
+__host__ __device__ __forceinline__ int sort_class(long long len) { return len <= 2048 ? 0 : (len <= 6144 ? 1 : 2); }
 constexpr int kSortLambda = 2;                        // mean keys per bucket
 constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
 constexpr int kLocalThreads = 512;    // CTA of the local partitioner
@@ -62,10 +67,8 @@ struct DevStatus {
     int nlocal[2];                    // local-partition segments (current round, next round)
     int nlocal_big[2];                // ... of which > kLocalBig keys (stored from the top of the list)
     int local_next;                   // dynamic work counter of the local round
-    int nsort;                        // segment-sorter list (<= kSortBig keys, from index 0 upwards)
-    int nsort_big;                    // ... > kSortBig keys (stored from the top of the list)
-    int sort_next;                    // dynamic work counters of the segment sorter (big, small lists)
-    int sort_next_small;
+    int nsort[kSortClasses];          // segment-sorter lists, one per size class
+    int sort_next[kSortClasses];      // dynamic work counters of the segment sorter
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
@@ -159,9 +162,11 @@ __device__ __forceinline__ int classify(double v, const double *piv, const unsig
     const unsigned e = lut[lut_bucket(v, lo, scale, T)];
     int a = (int)(e & 0xffffu);
     const int b = (int)(e >> 16);
-    if (a == b) return 2 * a;
+    if (a == b) return 2 * a;   // no pivot in the bucket: one shared-memory load in all
+    const double p0 = piv[a];
+    if (b - a == 1) return 2 * (a + (p0 < v ? 1 : 0)) + (p0 == v ? 1 : 0);
     if (b - a <= 3) {
-        const double p0 = piv[a], p1 = piv[a + 1], p2 = piv[a + 2], p3 = piv[a + 3];
+        const double p1 = piv[a + 1], p2 = piv[a + 2], p3 = piv[a + 3];
         const int r = a + (p0 < v) + (p1 < v) + (p2 < v);
         const int eq = (p0 == v) | (p1 == v) | (p2 == v) | (p3 == v);
         return 2 * r + eq;
@@ -210,6 +215,36 @@ __device__ __forceinline__ long long block_exclusive_scan(long long x, long long
     }
     __syncthreads();
     long long res = sh[wid] + inc - x;
+    if (total) *total = sh[32];
+    __syncthreads();
+    return res;
+}
+
+// 32-bit variant (same contract; `sh` needs 33 slots).
+__device__ __forceinline__ unsigned block_exclusive_scan_u32(unsigned x, unsigned *sh, unsigned *total)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    unsigned inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        const unsigned w = lane < nw ? sh[lane] : 0u;
+        unsigned winc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, winc, o);
+            if (lane >= o) winc += y;
+        }
+        if (lane < nw) sh[lane] = winc - w;
+        if (lane == 31) sh[32] = winc;
+    }
+    __syncthreads();
+    const unsigned res = sh[wid] + inc - x;
     if (total) *total = sh[32];
     __syncthreads();
     return res;
