@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libksort.so")
+LIB_PATH = os.environ.get("KSORT_LIB") or os.path.join(_HERE, "libksort.so")   # KSORT_LIB: experiment builds
 
 KS_OK = 0
 KS_NONFINITE = 1

@@ -46,7 +46,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     if not force and out is None and not needs_build():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    objdir = os.path.join(HERE, "build")
+    defs = os.environ.get("KS_DEFS", "").split()   # experiment variants: extra -D flags
+    objdir = os.path.join(HERE, "build", "v_" + "_".join(d.lstrip("-D").replace("=", "") for d in defs)) if defs \
+        else os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
              f'-DKS_GIT="{_git_rev()}"', *ARCH]
@@ -54,6 +56,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
         flags += ["-Xptxas", "-v"]
     if os.environ.get("KS_TRACE"):
         flags += ["-DKS_TRACE"]
+    flags += defs
     objs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))

@@ -44,6 +44,20 @@ __device__ unsigned long long g_trace[16];
 #define KS_TR(slot)
 #endif
 
+// build-time variants (experiments; defaults are the measured best)
+#ifndef KS_BATCH
+#define KS_BATCH 0        // batched (overlapped) classify in the count / scatter loops (measured: no gain)
+#endif
+#ifndef KS_SCATTER_EXP
+#define KS_SCATTER_EXP 0
+#endif
+#ifndef KS_PREFETCH
+#define KS_PREFETCH 1     // L2 prefetch of each chunk's scatter destinations
+#endif
+#ifndef KS_PASS_MINB
+#define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
+#endif
+
 constexpr int kScanBlock = 4096;   // count-matrix entries per scan CTA (512 thr x 8)
 constexpr int kScanThreads = 512;
 
@@ -417,7 +431,7 @@ struct CountSmem {
 };
 
 template <bool kGate>
-__global__ void __launch_bounds__(kCountThreads) k_count(const Seg *segs, const int *chunk_seg, const DevStatus *cst,
+__global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg *segs, const int *chunk_seg, const DevStatus *cst,
                                                          const double *src, const double *piv_pool,
                                                          const unsigned *lut_pool, unsigned *mat, DevStatus *st)
 {
@@ -451,11 +465,24 @@ __global__ void __launch_bounds__(kCountThreads) k_count(const Seg *segs, const 
             double v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) v[u] = in[i0 + u * kCountThreads];
+            if (kGate) {   // non-finite or zero keys are rare: check the batch, then look closer
+                bool odd = false;
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (kGate) gate_one(v[u], base + threadIdx.x + i0 + u * kCountThreads, bad, pz, nz);
-                atomicAdd(&hist[classify(v[u], P.piv, P.lut, lo, scale, T)], 1u);
+                for (int u = 0; u < U; ++u) odd |= !(fabs(v[u]) <= DBL_MAX) || v[u] == 0.0;
+                if (odd) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) gate_one(v[u], base + threadIdx.x + i0 + u * kCountThreads, bad, pz, nz);
+                }
             }
+#if KS_BATCH
+            int c[U];
+            classify_batch<U>(v, c, P.piv, P.lut, lo, scale, T);
+#pragma unroll
+            for (int u = 0; u < U; ++u) atomicAdd(&hist[c[u]], 1u);
+#else
+#pragma unroll
+            for (int u = 0; u < U; ++u) atomicAdd(&hist[classify(v[u], P.piv, P.lut, lo, scale, T)], 1u);
+#endif
         }
         for (int i = i0 + threadIdx.x; i < cnt; i += kCountThreads) {
             const double v = src[base + i];
@@ -551,10 +578,10 @@ struct ScatterSmem {
     Seg sg;
 };
 
-__global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const int *chunk_seg,
+__global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Seg *segs, const int *chunk_seg,
                                                           const DevStatus *cst, const double *src, double *dst,
                                                           const double *piv_pool, const unsigned *lut_pool,
-                                                          const long long *moff)
+                                                          const long long *moff, const unsigned *mat)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
@@ -576,21 +603,51 @@ __global__ void __launch_bounds__(kPassThreads) k_scatter(const Seg *segs, const
         const long long base_i = moff[g.mat_off];
         const int nch = g.nch, T = g.T;
         const double lo = g.lo, scale = g.scale;
-        for (int q = threadIdx.x; q <= g.k; q += blockDim.x)
-            S.cursor[q] = (unsigned)(moff[g.mat_off + (long long)(2 * q) * nch + j] - base_i);
+        double *out = dst + g.start;
+        for (int q = threadIdx.x; q <= g.k; q += blockDim.x) {
+            const long long e = g.mat_off + (long long)(2 * q) * nch + j;
+            const unsigned c0 = (unsigned)(moff[e] - base_i);
+            S.cursor[q] = c0;
+#if KS_PREFETCH
+            // pull this chunk's destination run of gap q into L2 ahead of the
+            // 8-byte stores (a partial-sector store that misses L2 waits for a fill)
+            l2_prefetch(out + c0, 8ull * mat[e]);
+#endif
+        }
         __syncthreads();
         const double *in = src + base + threadIdx.x;
-        double *out = dst + g.start;
         int i0 = 0;
         for (; i0 + U * kPassThreads <= cnt; i0 += U * kPassThreads) {
             double v[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) v[u] = in[i0 + u * kPassThreads];
+#if KS_BATCH
+            int c[U];
+            classify_batch<U>(v, c, S.P.piv, S.P.lut, lo, scale, T);
+            unsigned slot[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) slot[u] = (c[u] & 1) ? 0u : atomicAdd(&S.cursor[c[u] >> 1], 1u);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (!(c[u] & 1)) out[slot[u]] = v[u];
+#else
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int c = classify(v[u], S.P.piv, S.P.lut, lo, scale, T);
+#if KS_SCATTER_EXP == 1   // experiment: slots taken, stores coalesced (wrong output)
+                if (!(c & 1)) {
+                    const unsigned sl = atomicAdd(&S.cursor[c >> 1], 1u);
+                    out[(base - g.start) + i0 + u * kPassThreads + threadIdx.x] = v[u] + (double)(sl & 1);
+                }
+#elif KS_SCATTER_EXP == 2   // experiment: no slots, stores coalesced (wrong output)
+                if (!(c & 1)) out[(base - g.start) + i0 + u * kPassThreads + threadIdx.x] = v[u];
+#elif KS_SCATTER_EXP == 3   // experiment: slots taken, scattered stores of L2-resident lines (wrong output)
+                if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u) & 0x3fffff] = v[u];
+#else
                 if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u)] = v[u];
+#endif
             }
+#endif
         }
         for (int i = i0 + threadIdx.x; i < cnt; i += kPassThreads) {
             const double v = src[base + i];
@@ -721,7 +778,10 @@ __device__ __forceinline__ void account_partition(DevStatus *st, long long len, 
 // plan (global pass): class extents from the scanned count matrix
 // ---------------------------------------------------------------------------
 constexpr int kPlanThreads = 512;
+constexpr int kPlanChunks = (kPMax + 1 + kPlanThreads - 1) / kPlanThreads;   // grid.y: pivot-pair chunks
 
+// One CTA per (segment, chunk of kPlanThreads pivot pairs): gap 2j and
+// equality run 2j+1 for j in the chunk (j = k: the last gap).
 __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const int *nseg, const double *piv_pool,
                                                        const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
 {
@@ -729,33 +789,33 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
     __shared__ long long sbase[4 + kSortClasses];
     if (abort_requested(st)) return;
     const int ns = *nseg;
+    const int j0 = blockIdx.y * kPlanThreads;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
-        __syncthreads();
         const Seg g = segs[s];
+        if (j0 > g.k) continue;   // block-uniform
+        __syncthreads();
         const long long base_i = moff[g.mat_off];
-        EmitOut tot{0, 0, 0};
-        // pivot pairs (gap 2j, run 2j+1), kPlanThreads at a time
-        for (int j0 = 0; j0 <= g.k; j0 += kPlanThreads) {
-            const int j = j0 + threadIdx.x;
-            const bool have = j <= g.k;
-            long long ag = 0, gl = 0, ae = 0, el = 0;
-            double pv = 0.0;
-            if (have) {
-                ag = class_start(g, moff, base_i, 2 * j);
-                ae = class_start(g, moff, base_i, 2 * j + 1);
-                gl = ae - ag;
-                if (j < g.k) {
-                    el = class_start(g, moff, base_i, 2 * j + 2) - ae;
-                    pv = piv_pool[g.piv_off + j];
-                }
+        const int j = j0 + threadIdx.x;
+        const bool have = j <= g.k;
+        long long ag = 0, gl = 0, ae = 0, el = 0;
+        double pv = 0.0;
+        if (have) {
+            ag = class_start(g, moff, base_i, 2 * j);
+            ae = class_start(g, moff, base_i, 2 * j + 1);
+            gl = ae - ag;
+            if (j < g.k) {
+                el = class_start(g, moff, base_i, 2 * j + 2) - ae;
+                pv = piv_pool[g.piv_off + j];
             }
-            const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase,
-                                         (g.start << 8) | (A.tag_round & 0xff));
-            tot.unit_keys += o.unit_keys;
-            tot.fill_keys += o.fill_keys;
-            tot.items += o.items;
         }
-        if (threadIdx.x == 0) account_partition(st, g.len, tot, false);
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase,
+                                     (g.start << 8) | (A.tag_round & 0xff));
+        if (threadIdx.x == 0) {
+            // keys of this chunk's classes [2 j0, 2 min(j0 + kPlanThreads, k + 1))
+            const int jend = min(j0 + kPlanThreads, g.k + 1);
+            const long long len = class_start(g, moff, base_i, 2 * jend) - class_start(g, moff, base_i, 2 * j0);
+            account_partition(st, len, o, false);
+        }
     }
 }
 
@@ -1061,6 +1121,9 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 5))
             S.start = g.start;
             S.len = (int)g.len;
             S.src = g.src;
+#if KS_PREFETCH
+            l2_prefetch(keys + g.start, 8ull * g.len);
+#endif
         }
     }
     __syncthreads();
@@ -1225,6 +1288,12 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 5))
             S.len = nlen;
             S.src = nsrc;
             S.nbig = 0;
+#if KS_PREFETCH
+            if (nd < n) {   // next segment: its input and (when different) its output range
+                l2_prefetch((nsrc ? tmp : keys) + nstart, 8ull * nlen);
+                if (nsrc) l2_prefetch(keys + nstart, 8ull * nlen);
+            }
+#endif
         }
         __syncthreads();
     }
@@ -1494,10 +1563,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         K.run(kPhScan, [&] { k_scan_apply<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum, moff); });
         K.run(kPhScatter, [&] {
             k_scatter<<<g_scatter, kPassThreads, sizeof(ScatterSmem), stream>>>(segs[gcur], chunk_seg, st, src, dst, piv,
-                                                                               lut, moff);
+                                                                               lut, moff, mat);
         });
         cudaMemsetAsync(nseg_next, 0, sizeof(int), stream);
-        K.run(kPhPlan, [&] { k_plan<<<g_seg, kPlanThreads, 0, stream>>>(segs[gcur], nseg_cur, piv, moff, A, st, dst_id); });
+        K.run(kPhPlan, [&] {
+            k_plan<<<dim3(g_seg, kPlanChunks), kPlanThreads, 0, stream>>>(segs[gcur], nseg_cur, piv, moff, A, st, dst_id);
+        });
         cudaMemsetAsync(nseg_cur, 0, sizeof(int), stream);
         ++level;
         gcur ^= 1;

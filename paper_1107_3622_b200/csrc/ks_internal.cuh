@@ -179,6 +179,55 @@ __device__ __forceinline__ int classify(double v, const double *piv, const unsig
     return 2 * a + (piv[a] == v ? 1 : 0);
 }
 
+// Batched classify of U independent keys, written so that the U lookup
+// chains overlap: all LUT loads, then the first two pivots of every bucket,
+// then branch-free class arithmetic.  Buckets with more than two pivots
+// (rare when T >= 4P) are finished by the general classify.
+template <int U>
+__device__ __forceinline__ void classify_batch(const double (&v)[U], int (&c)[U], const double *piv,
+                                               const unsigned *lut, double lo, double scale, int T)
+{
+    unsigned e[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) e[u] = lut[lut_bucket(v[u], lo, scale, T)];
+    double p0[U], p1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int a = (int)(e[u] & 0xffffu);
+        p0[u] = piv[a];       // piv[k..k+3] are NaN sentinels: always in range
+        p1[u] = piv[a + 1];
+    }
+    unsigned slow = 0;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int a = (int)(e[u] & 0xffffu), d = (int)(e[u] >> 16) - a;
+        const bool h0 = d > 0, h1 = d > 1;
+        const int r = a + ((h0 && p0[u] < v[u]) ? 1 : 0) + ((h1 && p1[u] < v[u]) ? 1 : 0);
+        const int eq = ((h0 && p0[u] == v[u]) || (h1 && p1[u] == v[u])) ? 1 : 0;
+        c[u] = 2 * r + eq;
+        slow |= (d > 2 ? 1u : 0u) << u;
+    }
+    if (slow) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if ((slow >> u) & 1u) c[u] = classify(v[u], piv, lut, lo, scale, T);
+    }
+}
+
+// Asynchronous L2 prefetch of a byte range (TMA bulk prefetch; the range is
+// widened to 16-byte alignment).  Used ahead of scattered 8-byte stores: a
+// partial-sector store that misses L2 would otherwise wait for a DRAM fill.
+__device__ __forceinline__ void l2_prefetch(const void *p, unsigned long long bytes)
+{
+    if (bytes == 0) return;
+    const unsigned long long a0 = reinterpret_cast<unsigned long long>(p) & ~15ull;
+    const unsigned long long a1 = (reinterpret_cast<unsigned long long>(p) + bytes + 15ull) & ~15ull;
+    for (unsigned long long a = a0; a < a1; a += (1ull << 20)) {   // <= 1 MiB per instruction
+        const unsigned long long e = a1 - a < (1ull << 20) ? a1 - a : (1ull << 20);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((unsigned)e) : "memory");
+    }
+}
+
 __host__ __device__ __forceinline__ long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
 __host__ __device__ __forceinline__ int next_pow2(int x)
