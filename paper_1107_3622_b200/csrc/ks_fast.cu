@@ -316,22 +316,12 @@ __host__ __device__ __forceinline__ int lut_for(int P, int tmax)
 // ---------------------------------------------------------------------------
 // global pass bookkeeping
 // ---------------------------------------------------------------------------
-__global__ void k_seg_prep(Seg *segs, const int *nseg)
-{
-    int ns = *nseg;
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
-        Seg g = segs[s];
-        g.P = pivots_for(g.len, kPMax);
-        g.rows = 2 * g.P + 1;
-        g.nch = (int)cdiv(g.len, kChunk);
-        g.T = lut_for(g.P, kLutMax);
-        segs[s] = g;
-    }
-}
-
-// One CTA: exclusive scans over segments for pool offsets and matrix layout.
+// One CTA: per-segment pass shape (P, rows, chunks, LUT size) and exclusive
+// scans over segments for pool offsets and the count-matrix layout; then an
+// L2 prefetch of this level's count matrix and offsets (they are written with
+// scattered 4- and 8-byte stores).
 __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long long mat_cap, int ch_cap,
-                              int piv_cap, int lut_cap)
+                              int piv_cap, int lut_cap, const unsigned *mat, const long long *moff)
 {
     __shared__ long long sh[33];
     int ns = *nseg;
@@ -339,7 +329,13 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
     for (int base = 0; base < ns; base += blockDim.x) {
         int s = base + threadIdx.x;
         Seg g{};
-        if (s < ns) g = segs[s];
+        if (s < ns) {
+            g = segs[s];
+            g.P = pivots_for(g.len, kPMax);
+            g.rows = 2 * g.P + 1;
+            g.nch = (int)cdiv(g.len, kChunk);
+            g.T = lut_for(g.P, kLutMax);
+        }
         const bool in = s < ns;
         long long tp, tl, tm, tc;
         long long xp = block_exclusive_scan(in ? g.P + 1 : 0, sh, &tp);
@@ -367,6 +363,11 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
             st->overflow = 2;
             st->nchunks = 0;
             st->mat_total = 0;
+        } else {
+#if KS_PREFETCH
+            l2_prefetch(mat, 4ull * c_mat);
+            l2_prefetch(moff, 8ull * c_mat);
+#endif
         }
     }
 }
@@ -391,10 +392,13 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *
         const Seg g = segs[s];
         int k, T;
         double lo, scale;
+        KS_TR_DECL;
         build_pivots(src + g.start, g.P, g.T, piv, lut, W, k, T, lo, scale);
+        KS_TR(11);
         for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = piv[i];
         for (int t = threadIdx.x; t < T; t += blockDim.x) lut_pool[g.lut_off + t] = lut[t];
         for (int c = threadIdx.x; c < g.nch; c += blockDim.x) chunk_seg[g.ch_off + c] = s;
+        KS_TR(12);
         if (threadIdx.x == 0) {
             segs[s].k = k;
             segs[s].T = T;
@@ -736,9 +740,11 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         it.value = pv;
         if (ui < A.ucap) A.units[ui] = it; else st->overflow = 3;
     }
-    if (s_cls >= 0) {
+    if (s_cls >= 0) {   // static indexing of the argument arrays (no local-memory copy)
         const long long i = sbase[4 + s_cls] + pk_get(xpks, 20 * s_cls, 20);
-        if (i < A.scap[s_cls]) A.snext[s_cls][i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
+        Seg *list = s_cls == 0 ? A.snext[0] : (s_cls == 1 ? A.snext[1] : A.snext[2]);
+        const int cap = s_cls == 0 ? A.scap[0] : (s_cls == 1 ? A.scap[1] : A.scap[2]);
+        if (i < cap) list[i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
     }
     if (l_gap) {
         const long long li = sbase[1] + pk_get(xpk, kPkL, 10);
@@ -1478,7 +1484,6 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         g_sortc[2] = sms * (o2 > 0 ? o2 : 1);
     }
     const int g_scan = sms * 2;
-    const int g_seg = sms * 4;
     const int g_pivots = sms;
     Launcher K(stream, profile);
 
@@ -1539,16 +1544,19 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         double *dst = (level & 1) ? keys : tmp;
         const int dst_id = (level & 1) ? 0 : 1;
         int *nseg_cur = &st->nseg[gcur];
+        // segments at this level: known on the host at level 0, else bounded by the table size
+        const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
+        const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
                    {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
                    units, L.unit_cap, level};
-        K.run(kPhPivots, [&] { k_seg_prep<<<g_seg, 256, 0, stream>>>(segs[gcur], nseg_cur); });
         K.run(kPhPivots, [&] {
-            k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap);
+            k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap,
+                                                  mat, moff);
         });
         K.run(kPhPivots, [&] {
-            k_pivots<<<g_pivots, kPivotThreads, sizeof(PivotsSmem), stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
+            k_pivots<<<gx, kPivotThreads, sizeof(PivotsSmem), stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
         });
         if (level == 0)
             K.run(kPhCount, [&] {
@@ -1567,7 +1575,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         });
         cudaMemsetAsync(nseg_next, 0, sizeof(int), stream);
         K.run(kPhPlan, [&] {
-            k_plan<<<dim3(g_seg, kPlanChunks), kPlanThreads, 0, stream>>>(segs[gcur], nseg_cur, piv, moff, A, st, dst_id);
+            k_plan<<<dim3(gx, kPlanChunks), kPlanThreads, 0, stream>>>(segs[gcur], nseg_cur, piv, moff, A, st, dst_id);
         });
         cudaMemsetAsync(nseg_cur, 0, sizeof(int), stream);
         ++level;
