@@ -118,9 +118,15 @@ __device__ __forceinline__ void route_initial(long long a, long long len, const 
     }
 }
 
+// Single array: reset the status block and route the whole array (one launch).
 __global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
 {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    static_assert(sizeof(DevStatus) % 8 == 0, "status is cleared in 8-byte words");
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
+    for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    st->bad_index = kNoIndex;
     route_initial(0, n, Lst, st);
 }
 
@@ -689,6 +695,7 @@ struct EmitArgs {
     Item *units;
     int ucap;
     int tag_round;     // pass / round number: makes unit tags unique per partition
+    double *keys;      // user buffer: short equality runs are written here directly
 };
 
 // packed per-thread list counts for one block scan: units (<= 2 per thread,
@@ -708,7 +715,10 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         else if (gl <= kLocalMax) lb_gap = 1;
         else g_gap = 1;
     }
-    const int f_eq = (have && el > 0) ? 1 : 0;
+    // equality runs: short ones are written right here, long ones become fill items
+    if (have && el > 0 && el <= kFillDirect)
+        for (long long i = 0; i < el; ++i) A.keys[ae + i] = pv;
+    const int f_eq = (have && el > kFillDirect) ? 1 : 0;
     const int nu = u_gap + f_eq;
     const long long pk = ((long long)nu << kPkU) | ((long long)l_gap << kPkL) | ((long long)lb_gap << kPkLB) |
                          ((long long)g_gap << kPkG);
@@ -760,7 +770,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     }
     // keys in fills / units (block totals; segments < 2^31 keys)
     long long tk;
-    block_exclusive_scan((f_eq ? el : 0) | ((u_gap ? gl : 0) << 32), sh, &tk);
+    block_exclusive_scan((have ? el : 0) | ((u_gap ? gl : 0) << 32), sh, &tk);
     EmitOut o;
     o.unit_keys = tk >> 32;
     o.fill_keys = tk & 0xffffffffll;
@@ -1520,12 +1530,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         cudaMemsetAsync(&st->nunits, 0, sizeof(int), stream);
     };
 
-    KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
-    KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
+    if (d_off != nullptr) {   // (the single-array init kernel clears the status itself)
+        KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
+        KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
+    }
     const InitLists Lst{segs[0], lsegs[0], {ssegs[0], ssegs[1], ssegs[2]}, units, L.seg_cap, L.lseg_cap,
                         {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]}, L.unit_cap};
     if (d_off == nullptr) {
-        K.run(kPhGate, [&] { k_init_single<<<1, 32, 0, stream>>>(n, Lst, st); });
+        K.run(kPhGate, [&] { k_init_single<<<1, 64, 0, stream>>>(n, Lst, st); });
         if (n <= kLocalMax)
             K.run(kPhGate, [&] { k_gate_segments<<<sms * 2, 256, 0, stream>>>(keys, nullptr, 0, n, st); });
     } else {
@@ -1550,7 +1562,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         int *nseg_next = &st->nseg[gcur ^ 1];
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
                    {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
-                   units, L.unit_cap, level};
+                   units, L.unit_cap, level, keys};
         K.run(kPhPivots, [&] {
             k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap,
                                                   mat, moff);
@@ -1587,7 +1599,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
         EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
                    L.lseg_cap, {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
-                   units, L.unit_cap, 128 + rounds};
+                   units, L.unit_cap, 128 + rounds, keys};
         K.run(kPhOther, [&] {
             k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
                                                                            L.lseg_cap, A, st, keys, tmp);

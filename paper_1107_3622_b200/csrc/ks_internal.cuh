@@ -35,6 +35,7 @@ constexpr int kPassThreads = 512;     // threads of scatter CTAs (8 keys each pe
 constexpr int kLocalMax = 131072;     // segments <= this are partitioned by one CTA (L2-resident)
 constexpr int kLocalBig = 32768;      // local segments above this are scheduled first (LPT)
 constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
+constexpr int kFillDirect = 16;       // equality runs up to this are written by the emitting thread
 // segment sorter: one CTA sorts a whole segment on chip (shared-memory copy ->
 // interpolation buckets -> per-thread / per-warp bucket sorts).  Three size
 // classes, each with its own CTA shape so that every thread holds 12..16 keys:
