@@ -54,6 +54,9 @@ __device__ unsigned long long g_trace[16];
 #ifndef KS_PREFETCH
 #define KS_PREFETCH 1     // L2 prefetch of each chunk's scatter destinations
 #endif
+#ifndef KS_SCAN3
+#define KS_SCAN3 0        // 1: three-kernel count-matrix scan instead of the look-back scan
+#endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
 #endif
@@ -327,7 +330,8 @@ __host__ __device__ __forceinline__ int lut_for(int P, int tmax)
 // L2 prefetch of this level's count matrix and offsets (they are written with
 // scattered 4- and 8-byte stores).
 __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long long mat_cap, int ch_cap,
-                              int piv_cap, int lut_cap, const unsigned *mat, const long long *moff)
+                              int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
+                              unsigned long long *tstat)
 {
     __shared__ long long sh[33];
     int ns = *nseg;
@@ -375,7 +379,11 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
             l2_prefetch(moff, 8ull * c_mat);
 #endif
         }
+        st->scan_next = 0;
     }
+    // look-back words of the single-pass scan (c_mat is block-uniform)
+    const long long nt = c_mat <= mat_cap ? cdiv(c_mat, kScanBlock) : 0;
+    for (long long i = threadIdx.x; i < nt; i += blockDim.x) tstat[i] = 0ull;
 }
 
 struct PivotsSmem {
@@ -563,6 +571,98 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const unsigned *mat
             if (i0 + e < total) moff[i0 + e] = ex;
             ex += v[e];
         }
+    }
+}
+
+// Single-pass exclusive scan of the count matrix (decoupled look-back):
+// tiles are claimed in order from a counter; each publishes its aggregate,
+// then warp 0 walks back over the predecessors' published words (aggregate or
+// inclusive prefix) until it meets a prefix.  Word = flag << 62 | value.
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *mat, DevStatus *st,
+                                                                unsigned long long *tstat, long long *moff)
+{
+    constexpr unsigned long long kScanAgg = 1ull << 62, kScanPrefix = 2ull << 62, kScanVal = (1ull << 62) - 1;
+    __shared__ long long sh[33];
+    __shared__ int s_tile;
+    __shared__ long long s_excl;
+    constexpr int E = kScanBlock / kScanThreads;
+    static_assert(E == 8, "two uint4 per thread");
+    const long long total = st->mat_total;
+    const int ntiles = (int)cdiv(total, kScanBlock);
+    const int lane = threadIdx.x & 31;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(&st->scan_next, 1);
+        __syncthreads();
+        const int t = s_tile;
+        if (t >= ntiles) break;
+        const long long i0 = (long long)t * kScanBlock + (long long)threadIdx.x * E;
+        unsigned v[E];
+        if (i0 + E <= total) {
+            const uint4 a = *reinterpret_cast<const uint4 *>(mat + i0);
+            const uint4 b = *reinterpret_cast<const uint4 *>(mat + i0 + 4);
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) v[e] = i0 + e < total ? mat[i0 + e] : 0u;
+        }
+        long long s = 0;
+#pragma unroll
+        for (int e = 0; e < E; ++e) s += v[e];
+        long long tot;
+        long long ex = block_exclusive_scan(s, sh, &tot);
+        if (threadIdx.x < 32) {
+            long long excl = 0;
+            if (t == 0) {
+                if (lane == 0) *reinterpret_cast<volatile unsigned long long *>(&tstat[0]) = kScanPrefix | (unsigned long long)tot;
+            } else {
+                if (lane == 0) {
+                    __threadfence();
+                    *reinterpret_cast<volatile unsigned long long *>(&tstat[t]) = kScanAgg | (unsigned long long)tot;
+                }
+                for (int j = t - 1;; j -= 32) {
+                    const int idx = j - lane;
+                    unsigned long long w;
+                    do {
+                        w = kScanPrefix;
+                        if (idx >= 0) w = *reinterpret_cast<volatile unsigned long long *>(&tstat[idx]);
+                    } while (!__all_sync(0xffffffffu, (w >> 62) != 0));
+                    const unsigned pm = __ballot_sync(0xffffffffu, (w >> 62) == 2);
+                    const int stop = pm ? __ffs(pm) - 1 : 31;
+                    long long val = lane <= stop ? (long long)(w & kScanVal) : 0;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    excl += val;
+                    if (pm) break;
+                }
+                if (lane == 0) {
+                    __threadfence();
+                    *reinterpret_cast<volatile unsigned long long *>(&tstat[t]) =
+                        kScanPrefix | (unsigned long long)(excl + tot);
+                }
+            }
+            if (lane == 0) s_excl = excl;
+        }
+        __syncthreads();
+        ex += s_excl;
+        if (i0 + E <= total) {
+            long long o[E];
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                o[e] = ex;
+                ex += v[e];
+            }
+#pragma unroll
+            for (int e = 0; e < E; e += 2)
+                *reinterpret_cast<longlong2 *>(moff + i0 + e) = make_longlong2(o[e], o[e + 1]);
+        } else {
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                if (i0 + e < total) moff[i0 + e] = ex;
+                ex += v[e];
+            }
+        }
+        __syncthreads();   // s_tile / s_excl reuse
     }
 }
 
@@ -1565,7 +1665,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                    units, L.unit_cap, level, keys};
         K.run(kPhPivots, [&] {
             k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap,
-                                                  mat, moff);
+                                                  mat, moff, reinterpret_cast<unsigned long long *>(bsum));
         });
         K.run(kPhPivots, [&] {
             k_pivots<<<gx, kPivotThreads, sizeof(PivotsSmem), stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
@@ -1578,9 +1678,16 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             K.run(kPhCount, [&] {
                 k_count<false><<<g_count, kCountThreads, sizeof(CountSmem), stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
+#if KS_SCAN3
         K.run(kPhScan, [&] { k_scan_reduce<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum); });
         K.run(kPhScan, [&] { k_scan_bsums<<<1, 1024, 0, stream>>>(bsum, st); });
         K.run(kPhScan, [&] { k_scan_apply<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum, moff); });
+#else
+        K.run(kPhScan, [&] {
+            k_scan_lookback<<<g_scan, kScanThreads, 0, stream>>>(mat, st, reinterpret_cast<unsigned long long *>(bsum),
+                                                                 moff);
+        });
+#endif
         K.run(kPhScatter, [&] {
             k_scatter<<<g_scatter, kPassThreads, sizeof(ScatterSmem), stream>>>(segs[gcur], chunk_seg, st, src, dst, piv,
                                                                                lut, moff, mat);

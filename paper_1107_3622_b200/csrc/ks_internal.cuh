@@ -73,6 +73,7 @@ struct DevStatus {
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
+    int scan_next;                    // tile counter of the single-pass count-matrix scan
     int pad;
     unsigned long long bytes_moved;   // algorithmic bytes, all passes
     unsigned long long phase_bytes[8];  // per phase (ksort.h KS_FLAG_PROFILE numbering)
