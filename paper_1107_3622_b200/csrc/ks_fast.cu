@@ -437,9 +437,35 @@ __device__ __forceinline__ void load_seg(const Seg *segs, int s, const double *p
 {
     if (threadIdx.x == 0) sg = segs[s];
     __syncthreads();
-    for (int i = threadIdx.x; i < sg.k + kPivPad; i += blockDim.x)
-        P.piv[i] = i < sg.k ? piv_pool[sg.piv_off + i] : CUDART_NAN;
-    for (int i = threadIdx.x; i < sg.T; i += blockDim.x) P.lut[i] = lut_pool[sg.lut_off + i];
+    // copies unrolled by 8 so that the L2 loads overlap (a rolled copy waits
+    // one L2 round trip per element per thread)
+    const int np = sg.k + kPivPad, T = sg.T;
+    for (int i0 = 0; i0 < np; i0 += 8 * blockDim.x) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x + threadIdx.x;
+            x[u] = i < sg.k ? piv_pool[sg.piv_off + i] : CUDART_NAN;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x + threadIdx.x;
+            if (i < np) P.piv[i] = x[u];
+        }
+    }
+    for (int i0 = 0; i0 < T; i0 += 8 * blockDim.x) {
+        unsigned x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x + threadIdx.x;
+            x[u] = i < T ? lut_pool[sg.lut_off + i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * blockDim.x + threadIdx.x;
+            if (i < T) P.lut[i] = x[u];
+        }
+    }
 }
 
 struct CountSmem {
