@@ -740,15 +740,29 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
         const int nch = g.nch, T = g.T;
         const double lo = g.lo, scale = g.scale;
         double *out = dst + g.start;
-        for (int q = threadIdx.x; q <= g.k; q += blockDim.x) {
-            const long long e = g.mat_off + (long long)(2 * q) * nch + j;
-            const unsigned c0 = (unsigned)(moff[e] - base_i);
-            S.cursor[q] = c0;
+        for (int q0 = 0; q0 <= g.k; q0 += 4 * blockDim.x) {   // 4 gaps per thread in flight
+            long long off[4];
+            unsigned cnt[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * blockDim.x + threadIdx.x;
+                const long long e = g.mat_off + (long long)(2 * q) * nch + j;
+                off[u] = q <= g.k ? moff[e] : base_i;
+                cnt[u] = q <= g.k ? mat[e] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int q = q0 + u * blockDim.x + threadIdx.x;
+                if (q <= g.k) {
+                    const unsigned c0 = (unsigned)(off[u] - base_i);
+                    S.cursor[q] = c0;
 #if KS_PREFETCH
-            // pull this chunk's destination run of gap q into L2 ahead of the
-            // 8-byte stores (a partial-sector store that misses L2 waits for a fill)
-            l2_prefetch(out + c0, 8ull * mat[e]);
+                    // pull this chunk's destination run of gap q into L2 ahead of the
+                    // 8-byte stores (a partial-sector store that misses L2 waits for a fill)
+                    l2_prefetch(out + c0, 8ull * cnt[u]);
 #endif
+                }
+            }
         }
         __syncthreads();
         const double *in = src + base + threadIdx.x;
