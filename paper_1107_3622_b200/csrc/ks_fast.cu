@@ -19,6 +19,7 @@
 // one small status block per pass to decide whether another pass is needed.
 #include <cfloat>
 #include <cstdio>
+#include <mutex>
 #include <vector>
 
 #include "ks_host.h"
@@ -57,8 +58,27 @@ __device__ unsigned long long g_trace[16];
 #ifndef KS_SCAN3
 #define KS_SCAN3 0        // 1: three-kernel count-matrix scan instead of the look-back scan
 #endif
+#ifndef KS_PDL
+#define KS_PDL 1          // programmatic dependent launch between the engine's kernels
+#endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
+#endif
+
+// Every kernel of the fast engine starts here: wait until the preceding grid in
+// the stream has completed (its writes visible), then let the next grid's CTAs
+// be scheduled while this one runs (they wait at the same point).  This hides
+// the launch gap between the pipeline's dependent kernels.
+#if KS_PDL
+#define KS_PDL_ENTRY()                                            \
+    do {                                                          \
+        asm volatile("griddepcontrol.wait;" ::: "memory");        \
+        asm volatile("griddepcontrol.launch_dependents;" :::);    \
+    } while (0)
+#else
+#define KS_PDL_ENTRY() \
+    do {               \
+    } while (0)
 #endif
 
 constexpr int kScanBlock = 4096;   // count-matrix entries per scan CTA (512 thr x 8)
@@ -124,6 +144,7 @@ __device__ __forceinline__ void route_initial(long long a, long long len, const 
 // Single array: reset the status block and route the whole array (one launch).
 __global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
 {
+    KS_PDL_ENTRY();
     static_assert(sizeof(DevStatus) % 8 == 0, "status is cleared in 8-byte words");
     unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
     for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
@@ -135,6 +156,7 @@ __global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
 
 __global__ void k_init_segmented(const long long *off, long long nseg0, InitLists Lst, DevStatus *st)
 {
+    KS_PDL_ENTRY();
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nseg0;
          s += (long long)gridDim.x * blockDim.x) {
         const long long a = off[s], b = off[s + 1];
@@ -162,6 +184,7 @@ __device__ __forceinline__ void gate_flush(long long bad, unsigned pz, unsigned 
 __global__ void k_gate_segments(const double *keys, const long long *off, long long nseg0, long long n_single,
                                 DevStatus *st)
 {
+    KS_PDL_ENTRY();
     long long bad = LLONG_MAX;
     unsigned pz = 0, nz = 0;
     long long checked = 0;
@@ -331,8 +354,9 @@ __host__ __device__ __forceinline__ int lut_for(int P, int tmax)
 // scattered 4- and 8-byte stores).
 __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long long mat_cap, int ch_cap,
                               int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
-                              unsigned long long *tstat)
+                              unsigned long long *tstat, int *nseg_next)
 {
+    KS_PDL_ENTRY();
     __shared__ long long sh[33];
     int ns = *nseg;
     long long c_piv = 0, c_lut = 0, c_mat = 0, c_ch = 0;
@@ -380,6 +404,7 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
 #endif
         }
         st->scan_next = 0;
+        *nseg_next = 0;   // the plan of this pass appends the next level's segments
     }
     // look-back words of the single-pass scan (c_mat is block-uniform)
     const long long nt = c_mat <= mat_cap ? cdiv(c_mat, kScanBlock) : 0;
@@ -396,6 +421,7 @@ constexpr int kPivotThreads = 1024;
 __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *nseg, const double *src,
                                                           double *piv_pool, unsigned *lut_pool, int *chunk_seg)
 {
+    KS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     PivotsSmem &PS = *reinterpret_cast<PivotsSmem *>(smem_raw);
     auto &W = PS.W;
@@ -479,6 +505,7 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
                                                          const double *src, const double *piv_pool,
                                                          const unsigned *lut_pool, unsigned *mat, DevStatus *st)
 {
+    KS_PDL_ENTRY();
     constexpr int U = 8;   // keys in flight per lane
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CountSmem &CS = *reinterpret_cast<CountSmem *>(smem_raw);
@@ -545,6 +572,7 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
 __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const unsigned *mat, const DevStatus *st,
                                                               long long *bsum)
 {
+    KS_PDL_ENTRY();
     __shared__ long long sh[33];
     const long long total = st->mat_total;
     const long long nb = cdiv(total, kScanBlock);
@@ -562,6 +590,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_reduce(const unsigned *ma
 
 __global__ void __launch_bounds__(1024) k_scan_bsums(long long *bsum, const DevStatus *st)
 {
+    KS_PDL_ENTRY();
     __shared__ long long sh[33];
     const long long nb = cdiv(st->mat_total, kScanBlock);
     long long carry = 0;
@@ -578,6 +607,7 @@ __global__ void __launch_bounds__(1024) k_scan_bsums(long long *bsum, const DevS
 __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const unsigned *mat, const DevStatus *st,
                                                              const long long *bsum, long long *moff)
 {
+    KS_PDL_ENTRY();
     __shared__ long long sh[33];
     constexpr int E = kScanBlock / kScanThreads;
     const long long total = st->mat_total;
@@ -608,6 +638,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_apply(const unsigned *mat
 __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *mat, DevStatus *st,
                                                                 unsigned long long *tstat, long long *moff)
 {
+    KS_PDL_ENTRY();
     constexpr unsigned long long kScanAgg = 1ull << 62, kScanPrefix = 2ull << 62, kScanVal = (1ull << 62) - 1;
     __shared__ long long sh[33];
     __shared__ int s_tile;
@@ -719,6 +750,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
                                                           const double *piv_pool, const unsigned *lut_pool,
                                                           const long long *moff, const unsigned *mat)
 {
+    KS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     ScatterSmem &S = *reinterpret_cast<ScatterSmem *>(smem_raw);
     constexpr int U = 8;
@@ -941,6 +973,7 @@ constexpr int kPlanChunks = (kPMax + 1 + kPlanThreads - 1) / kPlanThreads;   // 
 __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const int *nseg, const double *piv_pool,
                                                        const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
 {
+    KS_PDL_ENTRY();
     __shared__ long long sh[33];
     __shared__ long long sbase[4 + kSortClasses];
     if (abort_requested(st)) return;
@@ -997,6 +1030,7 @@ __global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const
                                                          int lcap, EmitArgs A, DevStatus *st, double *keys,
                                                          double *tmp)
 {
+    KS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LocalSmem &L = *reinterpret_cast<LocalSmem *>(smem_raw);
     if (abort_requested(st)) return;
@@ -1123,6 +1157,7 @@ __device__ __forceinline__ void warp_unit_sort(const double *__restrict__ in, do
 __global__ void __launch_bounds__(kUnitWarps * 32, 3) k_finish_units(const Item *units, const DevStatus *cst,
                                                                      double *keys, const double *tmp)
 {
+    KS_PDL_ENTRY();
     __shared__ double sm_all[kUnitWarps][sidx_size(kUnitMax)];
     if (abort_requested(cst)) return;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1260,6 +1295,7 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 5))
     k_segsort(const Seg *list, const int *count, int *next, Seg *lnext, int *nlnext, int lcap, DevStatus *st,
               double *keys, const double *tmp)
 {
+    KS_PDL_ENTRY();
     using Smem = SortSmem<kT, kCap>;
     constexpr int kWarps = kT / 32;
     static_assert(Smem::kPB * kT == Smem::kBuckets, "whole buckets per thread");
@@ -1537,6 +1573,38 @@ class Launcher {
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
+// Launch with programmatic stream serialization (PDL): the kernel may be
+// scheduled while its predecessor runs; KS_PDL_ENTRY() in every kernel waits
+// for the predecessor's completion before touching its results.
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                          Args &&...args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = KS_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// Small reset kernel (replaces memset nodes, which would break the PDL chain).
+__global__ void k_set_ints(int *p0, int *p1, int *p2, int *p3)
+{
+    KS_PDL_ENTRY();
+    if (threadIdx.x == 0) {
+        if (p0) *p0 = 0;
+        if (p1) *p1 = 0;
+        if (p2) *p2 = 0;
+        if (p3) *p3 = 0;
+    }
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 FastLayout fast_layout(long long n, long long nseg0)
@@ -1579,6 +1647,56 @@ FastLayout fast_layout(long long n, long long nseg0)
     return L;
 }
 
+// Per-device launch shapes and kernel attributes, set up once per process
+// (cudaFuncSetAttribute / occupancy queries cost host time on every call).
+struct EngineCfg {
+    int sms, g_count, g_scatter, g_units, g_local, g_sortc[kSortClasses];
+};
+
+static const EngineCfg *engine_cfg()
+{
+    static std::mutex mu;
+    static EngineCfg cfgs[64];
+    static bool ready[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (ready[dev]) return &cfgs[dev];
+    EngineCfg c{};
+    bool ok = true;
+    auto smem = [&](auto kern, size_t bytes) {
+        ok = ok && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
+    };
+    smem(k_scatter, sizeof(ScatterSmem));
+    smem(k_local, sizeof(LocalSmem));
+    smem(k_pivots, sizeof(PivotsSmem));
+    smem(k_count<true>, sizeof(CountSmem));
+    smem(k_count<false>, sizeof(CountSmem));
+    smem(k_segsort<sort_threads(0), sort_cap(0)>, sizeof(SortSmem<sort_threads(0), sort_cap(0)>));
+    smem(k_segsort<sort_threads(1), sort_cap(1)>, sizeof(SortSmem<sort_threads(1), sort_cap(1)>));
+    smem(k_segsort<sort_threads(2), sort_cap(2)>, sizeof(SortSmem<sort_threads(2), sort_cap(2)>));
+    if (!ok) {
+        fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
+        return nullptr;
+    }
+    c.sms = sm_count();
+    auto grid = [&](auto kern, int threads, size_t bytes) {
+        int occ = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, bytes);
+        return c.sms * (occ > 0 ? occ : 1);
+    };
+    c.g_count = grid(k_count<false>, kCountThreads, sizeof(CountSmem));
+    c.g_scatter = grid(k_scatter, kPassThreads, sizeof(ScatterSmem));
+    c.g_units = grid(k_finish_units, kUnitWarps * 32, 0);
+    c.g_local = grid(k_local, kLocalThreads, sizeof(LocalSmem));
+    c.g_sortc[0] = grid(k_segsort<sort_threads(0), sort_cap(0)>, sort_threads(0), sizeof(SortSmem<sort_threads(0), sort_cap(0)>));
+    c.g_sortc[1] = grid(k_segsort<sort_threads(1), sort_cap(1)>, sort_threads(1), sizeof(SortSmem<sort_threads(1), sort_cap(1)>));
+    c.g_sortc[2] = grid(k_segsort<sort_threads(2), sort_cap(2)>, sort_threads(2), sizeof(SortSmem<sort_threads(2), sort_cap(2)>));
+    cfgs[dev] = c;
+    ready[dev] = true;
+    return &cfgs[dev];
+}
+
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
               cudaStream_t stream, bool profile, FastResult *res)
 {
@@ -1599,40 +1717,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     Item *units = reinterpret_cast<Item *>(w + L.o_units);
     double *tmp = reinterpret_cast<double *>(w + L.o_tmp);
 
-    KS_CK(cudaFuncSetAttribute(k_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ScatterSmem)));
-    KS_CK(cudaFuncSetAttribute(k_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LocalSmem)));
-    KS_CK(cudaFuncSetAttribute(k_pivots, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PivotsSmem)));
-    KS_CK(cudaFuncSetAttribute(k_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
-    KS_CK(cudaFuncSetAttribute(k_count<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CountSmem)));
-    KS_CK(cudaFuncSetAttribute(k_segsort<sort_threads(0), sort_cap(0)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(SortSmem<sort_threads(0), sort_cap(0)>)));
-    KS_CK(cudaFuncSetAttribute(k_segsort<sort_threads(1), sort_cap(1)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(SortSmem<sort_threads(1), sort_cap(1)>)));
-    KS_CK(cudaFuncSetAttribute(k_segsort<sort_threads(2), sort_cap(2)>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)sizeof(SortSmem<sort_threads(2), sort_cap(2)>)));
-    const int sms = sm_count();
-    int occ_count = 1, occ_scatter = 1, occ_units = 1, occ_local = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_count, k_count<false>, kCountThreads, sizeof(CountSmem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_scatter, k_scatter, kPassThreads, sizeof(ScatterSmem));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_units, k_finish_units, kUnitWarps * 32, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_local, k_local, kLocalThreads, sizeof(LocalSmem));
-    const int g_count = sms * (occ_count > 0 ? occ_count : 1);
-    const int g_scatter = sms * (occ_scatter > 0 ? occ_scatter : 1);
-    const int g_units = sms * (occ_units > 0 ? occ_units : 1);
-    const int g_local = sms * (occ_local > 0 ? occ_local : 1);
-    int g_sortc[kSortClasses];
-    {
-        int o0 = 1, o1 = 1, o2 = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o0, k_segsort<sort_threads(0), sort_cap(0)>, sort_threads(0),
-                                                      sizeof(SortSmem<sort_threads(0), sort_cap(0)>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_segsort<sort_threads(1), sort_cap(1)>, sort_threads(1),
-                                                      sizeof(SortSmem<sort_threads(1), sort_cap(1)>));
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_segsort<sort_threads(2), sort_cap(2)>, sort_threads(2),
-                                                      sizeof(SortSmem<sort_threads(2), sort_cap(2)>));
-        g_sortc[0] = sms * (o0 > 0 ? o0 : 1);
-        g_sortc[1] = sms * (o1 > 0 ? o1 : 1);
-        g_sortc[2] = sms * (o2 > 0 ? o2 : 1);
-    }
+    const EngineCfg *cfg = engine_cfg();
+    if (cfg == nullptr) return KS_CUDA_ERROR;
+    const int sms = cfg->sms;
+    const int g_count = cfg->g_count, g_scatter = cfg->g_scatter, g_units = cfg->g_units, g_local = cfg->g_local;
+    const int *g_sortc = cfg->g_sortc;
     const int g_scan = sms * 2;
     const int g_pivots = sms;
     Launcher K(stream, profile);
@@ -1648,26 +1737,20 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     int lc = 0;
     auto flush_units = [&]() {
         // segment sorter first: its rare hand-backs go to the current local list
-        cudaMemsetAsync(st->sort_next, 0, sizeof(st->sort_next), stream);
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->sort_next[0], &st->sort_next[1], &st->sort_next[2],
+               (int *)nullptr);
         // largest class first: its CTAs hold a whole SM each
         K.run(kPhLeaf, [&] {
-            k_segsort<sort_threads(2), sort_cap(2)><<<g_sortc[2], sort_threads(2), sizeof(SortSmem<sort_threads(2), sort_cap(2)>),
-                                                      stream>>>(ssegs[2], &st->nsort[2], &st->sort_next[2], lsegs[lc],
-                                                                &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            launch(k_segsort<sort_threads(2), sort_cap(2)>, dim3(g_sortc[2]), dim3(sort_threads(2)), sizeof(SortSmem<sort_threads(2), sort_cap(2)>), stream, ssegs[2], &st->nsort[2], &st->sort_next[2], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] {
-            k_segsort<sort_threads(1), sort_cap(1)><<<g_sortc[1], sort_threads(1), sizeof(SortSmem<sort_threads(1), sort_cap(1)>),
-                                                      stream>>>(ssegs[1], &st->nsort[1], &st->sort_next[1], lsegs[lc],
-                                                                &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            launch(k_segsort<sort_threads(1), sort_cap(1)>, dim3(g_sortc[1]), dim3(sort_threads(1)), sizeof(SortSmem<sort_threads(1), sort_cap(1)>), stream, ssegs[1], &st->nsort[1], &st->sort_next[1], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] {
-            k_segsort<sort_threads(0), sort_cap(0)><<<g_sortc[0], sort_threads(0), sizeof(SortSmem<sort_threads(0), sort_cap(0)>),
-                                                      stream>>>(ssegs[0], &st->nsort[0], &st->sort_next[0], lsegs[lc],
-                                                                &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            launch(k_segsort<sort_threads(0), sort_cap(0)>, dim3(g_sortc[0]), dim3(sort_threads(0)), sizeof(SortSmem<sort_threads(0), sort_cap(0)>), stream, ssegs[0], &st->nsort[0], &st->sort_next[0], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
-        cudaMemsetAsync(st->nsort, 0, sizeof(st->nsort), stream);
-        K.run(kPhLeaf, [&] { k_finish_units<<<g_units, kUnitWarps * 32, 0, stream>>>(units, st, keys, tmp); });
-        cudaMemsetAsync(&st->nunits, 0, sizeof(int), stream);
+        K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nsort[0], &st->nsort[1], &st->nsort[2], &st->nunits);
     };
 
     if (d_off != nullptr) {   // (the single-array init kernel clears the status itself)
@@ -1677,12 +1760,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const InitLists Lst{segs[0], lsegs[0], {ssegs[0], ssegs[1], ssegs[2]}, units, L.seg_cap, L.lseg_cap,
                         {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]}, L.unit_cap};
     if (d_off == nullptr) {
-        K.run(kPhGate, [&] { k_init_single<<<1, 64, 0, stream>>>(n, Lst, st); });
+        K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
         if (n <= kLocalMax)
-            K.run(kPhGate, [&] { k_gate_segments<<<sms * 2, 256, 0, stream>>>(keys, nullptr, 0, n, st); });
+            K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
     } else {
-        K.run(kPhGate, [&] { k_init_segmented<<<sms, 256, 0, stream>>>(d_off, nseg0, Lst, st); });
-        K.run(kPhGate, [&] { k_gate_segments<<<sms * 4, 256, 0, stream>>>(keys, d_off, nseg0, 0, st); });
+        K.run(kPhGate, [&] { launch(k_init_segmented, dim3(sms), dim3(256), 0, stream, d_off, nseg0, Lst, st); });
+        K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 4), dim3(256), 0, stream, keys, d_off, nseg0, 0, st); });
     }
 
     // The schedule is launched speculatively without host round-trips: global
@@ -1704,55 +1787,46 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                    {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
                    units, L.unit_cap, level, keys};
         K.run(kPhPivots, [&] {
-            k_seg_offsets<<<1, 1024, 0, stream>>>(segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap,
-                                                  mat, moff, reinterpret_cast<unsigned long long *>(bsum));
+            launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next);
         });
         K.run(kPhPivots, [&] {
-            k_pivots<<<gx, kPivotThreads, sizeof(PivotsSmem), stream>>>(segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
+            launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
         });
         if (level == 0)
             K.run(kPhCount, [&] {
-                k_count<true><<<g_count, kCountThreads, sizeof(CountSmem), stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
+                launch(k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
         else
             K.run(kPhCount, [&] {
-                k_count<false><<<g_count, kCountThreads, sizeof(CountSmem), stream>>>(segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
+                launch(k_count<false>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
             });
 #if KS_SCAN3
-        K.run(kPhScan, [&] { k_scan_reduce<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum); });
-        K.run(kPhScan, [&] { k_scan_bsums<<<1, 1024, 0, stream>>>(bsum, st); });
-        K.run(kPhScan, [&] { k_scan_apply<<<g_scan, kScanThreads, 0, stream>>>(mat, st, bsum, moff); });
+        K.run(kPhScan, [&] { launch(k_scan_reduce, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st, bsum); });
+        K.run(kPhScan, [&] { launch(k_scan_bsums, dim3(1), dim3(1024), 0, stream, bsum, st); });
+        K.run(kPhScan, [&] { launch(k_scan_apply, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st, bsum, moff); });
 #else
         K.run(kPhScan, [&] {
-            k_scan_lookback<<<g_scan, kScanThreads, 0, stream>>>(mat, st, reinterpret_cast<unsigned long long *>(bsum),
-                                                                 moff);
+            launch(k_scan_lookback, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st, reinterpret_cast<unsigned long long *>(bsum), moff);
         });
 #endif
         K.run(kPhScatter, [&] {
-            k_scatter<<<g_scatter, kPassThreads, sizeof(ScatterSmem), stream>>>(segs[gcur], chunk_seg, st, src, dst, piv,
-                                                                               lut, moff, mat);
+            launch(k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur], chunk_seg, st, src, dst, piv, lut, moff, mat);
         });
-        cudaMemsetAsync(nseg_next, 0, sizeof(int), stream);
         K.run(kPhPlan, [&] {
-            k_plan<<<dim3(gx, kPlanChunks), kPlanThreads, 0, stream>>>(segs[gcur], nseg_cur, piv, moff, A, st, dst_id);
+            launch(k_plan, dim3(dim3(gx, kPlanChunks)), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A, st, dst_id);
         });
-        cudaMemsetAsync(nseg_cur, 0, sizeof(int), stream);
         ++level;
         gcur ^= 1;
     };
     auto local_round = [&]() {
-        cudaMemsetAsync(&st->local_next, 0, sizeof(int), stream);
-        cudaMemsetAsync(&st->nlocal[lc ^ 1], 0, sizeof(int), stream);
-        cudaMemsetAsync(&st->nlocal_big[lc ^ 1], 0, sizeof(int), stream);
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->local_next, &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
+               (int *)nullptr);
         EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
                    L.lseg_cap, {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
                    units, L.unit_cap, 128 + rounds, keys};
         K.run(kPhOther, [&] {
-            k_local<<<g_local, kLocalThreads, sizeof(LocalSmem), stream>>>(lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc],
-                                                                           L.lseg_cap, A, st, keys, tmp);
+            launch(k_local, dim3(g_local), dim3(kLocalThreads), sizeof(LocalSmem), stream, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap, A, st, keys, tmp);
         });
-        cudaMemsetAsync(&st->nlocal[lc], 0, sizeof(int), stream);
-        cudaMemsetAsync(&st->nlocal_big[lc], 0, sizeof(int), stream);
         lc ^= 1;
         ++rounds;
     };
