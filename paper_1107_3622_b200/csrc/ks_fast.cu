@@ -1212,9 +1212,10 @@ __global__ void __launch_bounds__(kUnitWarps * 32, 3) k_finish_units(const Item 
 //      depend on the value distribution
 //   4. coalesced write-back.
 // ---------------------------------------------------------------------------
-template <int kT, int kCap>
+template <int C>
 struct SortSmem {
-    static constexpr int kBuckets = kCap / kSortLambda;     // interpolation buckets
+    static constexpr int kT = sort_threads(C), kCap = sort_cap(C), kLam = sort_lambda(C);
+    static constexpr int kBuckets = kCap / kLam;            // interpolation buckets
     static constexpr int kPB = kBuckets / kT;               // buckets per thread in the scan
     static constexpr int kBigCap = kCap / (kThreadSortMax + 1) + 1;
     double a[kCap];        // the segment as loaded
@@ -1290,13 +1291,15 @@ __device__ __noinline__ bool warp_sort_bucket(double *a, int sz)
 // pulled from a work counter; thread 0 prefetches the next descriptor while
 // the block works on the current one.  The per-segment code path is kept
 // short (no unrolled remainders): segments hold only ~10 keys per thread.
-template <int kT, int kCap>
-__global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 5))
+template <int C>
+__global__ void __launch_bounds__(sort_threads(C),
+                                  sort_threads(C) >= 1024 ? 1 : (sort_threads(C) >= 512 ? 2 : (sort_threads(C) >= 256 ? 3 : 5)))
     k_segsort(const Seg *list, const int *count, int *next, Seg *lnext, int *nlnext, int lcap, DevStatus *st,
               double *keys, const double *tmp)
 {
     KS_PDL_ENTRY();
-    using Smem = SortSmem<kT, kCap>;
+    using Smem = SortSmem<C>;
+    constexpr int kT = Smem::kT;
     constexpr int kWarps = kT / 32;
     static_assert(Smem::kPB * kT == Smem::kBuckets, "whole buckets per thread");
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1369,7 +1372,7 @@ __global__ void __launch_bounds__(kT, kT >= 1024 ? 1 : (kT >= 512 ? 2 : 5))
             S.red[0][wid] = mn;
             S.red[1][wid] = mx;
         }
-        int B = m / kSortLambda;
+        int B = m / Smem::kLam;
         B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
 #pragma unroll 1
         for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
@@ -1672,9 +1675,9 @@ static const EngineCfg *engine_cfg()
     smem(k_pivots, sizeof(PivotsSmem));
     smem(k_count<true>, sizeof(CountSmem));
     smem(k_count<false>, sizeof(CountSmem));
-    smem(k_segsort<sort_threads(0), sort_cap(0)>, sizeof(SortSmem<sort_threads(0), sort_cap(0)>));
-    smem(k_segsort<sort_threads(1), sort_cap(1)>, sizeof(SortSmem<sort_threads(1), sort_cap(1)>));
-    smem(k_segsort<sort_threads(2), sort_cap(2)>, sizeof(SortSmem<sort_threads(2), sort_cap(2)>));
+    smem(k_segsort<0>, sizeof(SortSmem<0>));
+    smem(k_segsort<1>, sizeof(SortSmem<1>));
+    smem(k_segsort<2>, sizeof(SortSmem<2>));
     if (!ok) {
         fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
         return nullptr;
@@ -1689,9 +1692,9 @@ static const EngineCfg *engine_cfg()
     c.g_scatter = grid(k_scatter, kPassThreads, sizeof(ScatterSmem));
     c.g_units = grid(k_finish_units, kUnitWarps * 32, 0);
     c.g_local = grid(k_local, kLocalThreads, sizeof(LocalSmem));
-    c.g_sortc[0] = grid(k_segsort<sort_threads(0), sort_cap(0)>, sort_threads(0), sizeof(SortSmem<sort_threads(0), sort_cap(0)>));
-    c.g_sortc[1] = grid(k_segsort<sort_threads(1), sort_cap(1)>, sort_threads(1), sizeof(SortSmem<sort_threads(1), sort_cap(1)>));
-    c.g_sortc[2] = grid(k_segsort<sort_threads(2), sort_cap(2)>, sort_threads(2), sizeof(SortSmem<sort_threads(2), sort_cap(2)>));
+    c.g_sortc[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
+    c.g_sortc[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
+    c.g_sortc[2] = grid(k_segsort<2>, sort_threads(2), sizeof(SortSmem<2>));
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -1741,13 +1744,13 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                (int *)nullptr);
         // largest class first: its CTAs hold a whole SM each
         K.run(kPhLeaf, [&] {
-            launch(k_segsort<sort_threads(2), sort_cap(2)>, dim3(g_sortc[2]), dim3(sort_threads(2)), sizeof(SortSmem<sort_threads(2), sort_cap(2)>), stream, ssegs[2], &st->nsort[2], &st->sort_next[2], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            launch(k_segsort<2>, dim3(g_sortc[2]), dim3(sort_threads(2)), sizeof(SortSmem<2>), stream, ssegs[2], &st->nsort[2], &st->sort_next[2], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] {
-            launch(k_segsort<sort_threads(1), sort_cap(1)>, dim3(g_sortc[1]), dim3(sort_threads(1)), sizeof(SortSmem<sort_threads(1), sort_cap(1)>), stream, ssegs[1], &st->nsort[1], &st->sort_next[1], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            launch(k_segsort<1>, dim3(g_sortc[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, ssegs[1], &st->nsort[1], &st->sort_next[1], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] {
-            launch(k_segsort<sort_threads(0), sort_cap(0)>, dim3(g_sortc[0]), dim3(sort_threads(0)), sizeof(SortSmem<sort_threads(0), sort_cap(0)>), stream, ssegs[0], &st->nsort[0], &st->sort_next[0], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
+            launch(k_segsort<0>, dim3(g_sortc[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, ssegs[0], &st->nsort[0], &st->sort_next[0], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
         launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nsort[0], &st->nsort[1], &st->nsort[2], &st->nunits);

@@ -42,12 +42,24 @@ constexpr int kFillDirect = 16;       // equality runs up to this are written by
 //   class 0: <= 2048 keys, 128 threads;  class 1: <= 6144, 512;  class 2: <= 12288, 1024
 constexpr int kSortClasses = 3;
 constexpr int kSortMax = 12288;
+#ifndef KS_T0
+#define KS_T0 128
+#endif
+#ifndef KS_LAM0
+#define KS_LAM0 2
+#endif
+#ifndef KS_LAM1
+#define KS_LAM1 2
+#endif
 __host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? 2048 : (c == 1 ? 6144 : kSortMax); }
-__host__ __device__ constexpr int sort_threads(int c) { return c == 0 ? 128 : (c == 1 ? 512 : 1024); }
+__host__ __device__ constexpr int sort_threads(int c) { return c == 0 ? KS_T0 : (c == 1 ? 512 : 1024); }
+__host__ __device__ constexpr int sort_lambda(int c) { return c == 0 ? KS_LAM0 : (c == 1 ? KS_LAM1 : 2); }   // keys per bucket
 __host__ __device__ __forceinline__ int sort_class(long long len) { return len <= 2048 ? 0 : (len <= 6144 ? 1 : 2); }
-constexpr int kSortLambda = 2;                        // mean keys per bucket
 constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
-constexpr int kLocalThreads = 512;    // CTA of the local partitioner
+#ifndef KS_LOCAL_THREADS
+#define KS_LOCAL_THREADS 512
+#endif
+constexpr int kLocalThreads = KS_LOCAL_THREADS;   // CTA of the local partitioner
 constexpr int kUnitWarps = 8;         // warps per CTA of the unit sorter
 
 constexpr unsigned long long kNoIndex = ~0ull;

@@ -1,4 +1,4 @@
-"""Phase cycles of k_finish per piece (needs scripts/libksort_trace.so built with KS_TRACE=1)."""
+"""Phase cycles of the local partitioner per segment (needs exp/lib_trace.so: scripts/exp_build.sh trace -DKS_TRACE)."""
 import ctypes
 import os
 import sys
@@ -6,7 +6,8 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_1107_3622_b200 import _lib  # noqa: E402
 
-L = _lib.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libksort_trace.so"))
+os.environ["KSORT_LIB"] = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "exp", "lib_trace.so")
+L = _lib.load(os.environ["KSORT_LIB"])
 import torch  # noqa: E402
 
 import paper_1107_3622_b200 as K  # noqa: E402
@@ -23,7 +24,7 @@ for rep in range(3):
     torch.cuda.synchronize()
     L.ks_trace_read(ctypes.addressof(buf), 16, 0)
     segs, keys = buf[4], buf[5]
-    print("rep %d: %d pieces (> 512 keys), %d keys; cycles/piece: load+pivots %.0f classify %.0f scan+perm %.0f "
-          "sort-units %.0f; cycles/key: classify %.2f sort %.2f" % (
-              rep, segs, keys, buf[0] / max(segs, 1), buf[1] / max(segs, 1), buf[2] / max(segs, 1),
-              buf[3] / max(segs, 1), buf[1] / max(keys, 1), buf[3] / max(keys, 1)))
+    print("rep %d: %d local segments, %d keys (%.0f/seg); cycles/seg: pivots %.0f count %.0f scatter %.0f emit %.0f; "
+          "cycles/key: count %.2f scatter %.2f" % (
+              rep, segs, keys, keys / max(segs, 1), buf[0] / max(segs, 1), buf[1] / max(segs, 1), buf[2] / max(segs, 1),
+              buf[3] / max(segs, 1), buf[1] / max(keys, 1), buf[2] / max(keys, 1)))
