@@ -87,14 +87,13 @@ constexpr int kScanThreads = 512;
 // ---------------------------------------------------------------------------
 // work lists
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ Item make_item(long long start, long long len, int kind, int src, long long tag = -1)
+__device__ __forceinline__ Item make_item(long long start, long long len, int kind, int src)
 {
     Item it{};
     it.start = start;
-    it.tag = tag;
     it.len = (int)len;
-    it.kind = kind;
-    it.src = src;
+    it.kind = (short)kind;
+    it.src = (short)src;
     return it;
 }
 
@@ -107,31 +106,91 @@ __device__ __forceinline__ Seg make_seg(long long start, long long len, int src)
     return g;
 }
 
-// Initial work lists (the first global / local round's tables).
-struct InitLists {
-    Seg *gsegs, *lsegs, *ssegs[kSortClasses];
-    Item *units;
-    int seg_cap, lseg_cap, sseg_cap[kSortClasses], unit_cap;
+// Work queues of the leaf kernel.  Producers (the global plan, the local
+// partitioner, the segment sorter's hand-back) raise `pending`, claim a slot,
+// write the item and publish it by storing the tag (epoch << 32 | claim) into
+// the slot's ready word; consumers claim in order and wait for that tag.
+// The queues are circular: items still queued are disjoint ranges of more
+// than kUnitMax keys (a parent leaves the queue before its children enter),
+// so cap >= n / (kUnitMax + 1) + (CTAs in flight) never overwrites a slot
+// that has not been read.
+struct LeafQ {
+    Seg *lq;          // local partitions (kSortMax < len <= kLocalMax)
+    unsigned long long *lq_ready;
+    int lcap;
+    Seg *sq;          // segment sorts (kUnitMax < len <= kSortMax)
+    unsigned long long *sq_ready;
+    int scap;
+    int epoch;        // leaf launch these items belong to
 };
 
-// Route one segment at start: > kLocalMax keys -> global pass list,
-// kSortMax < len <= kLocalMax -> local-partition list, kUnitMax < len <=
-// kSortMax -> segment sorter, 2..kUnitMax -> unit.
+__device__ __forceinline__ unsigned long long q_tag(int epoch, int idx)
+{
+    return ((unsigned long long)(unsigned)epoch << 32) | (unsigned)idx;
+}
+
+__device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int ld_acquire_s32(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// write the item, then release its tag (the item is visible before the tag)
+__device__ __forceinline__ void q_publish(Seg *q, unsigned long long *ready, int cap, int idx, const Seg &g,
+                                          int epoch)
+{
+    const int slot = idx % cap;
+    q[slot] = g;
+    st_release_u64(&ready[slot], q_tag(epoch, idx));
+}
+
+// The local queue holds only the global plan's items (all published before
+// the leaf launch starts).  Items made during the launch -- segments to sort,
+// local children still too large to sort on chip, the sorter's hand-backs --
+// go to the sort queue, each tagged with its kind.
+constexpr int kItemLocal = 0, kItemSort = 1;
+__device__ __forceinline__ Seg with_kind(Seg g, int kind)
+{
+    g.k = kind;
+    return g;
+}
+
+// single-item push to the sort queue (pending is raised before the slot can be claimed)
+__device__ __forceinline__ void q_push1(bool local, const LeafQ &Q, const Seg &g, DevStatus *st)
+{
+    atomicAdd(&st->pending, 1);
+    q_publish(Q.sq, Q.sq_ready, Q.scap, atomicAdd(&st->sq_claim, 1), with_kind(g, local ? kItemLocal : kItemSort),
+              Q.epoch);
+}
+
+// Initial routing of one array (or one segment of a batch).
+struct InitLists {
+    Seg *gsegs;
+    LeafQ Q;
+    Item *units;
+    int seg_cap, unit_cap;
+};
+
+// > kLocalMax keys -> global pass list, kSortMax < len <= kLocalMax -> local
+// queue, kUnitMax < len <= kSortMax -> sort queue, 2..kUnitMax -> unit.
 __device__ __forceinline__ void route_initial(long long a, long long len, const InitLists &Lst, DevStatus *st)
 {
     if (len > kLocalMax) {
         int i = atomicAdd(&st->nseg[0], 1);
         if (i < Lst.seg_cap) Lst.gsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
-    } else if (len > kLocalBig) {
-        int i = atomicAdd(&st->nlocal_big[0], 1);
-        if (i < Lst.lseg_cap) Lst.lsegs[Lst.lseg_cap - 1 - i] = make_seg(a, len, 0); else st->overflow = 1;
-    } else if (len > kSortMax) {
-        int i = atomicAdd(&st->nlocal[0], 1);
-        if (i < Lst.lseg_cap) Lst.lsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
     } else if (len > kUnitMax) {
-        const int c = sort_class(len);
-        int i = atomicAdd(&st->nsort[c], 1);
-        if (i < Lst.sseg_cap[c]) Lst.ssegs[c][i] = make_seg(a, len, 0); else st->overflow = 1;
+        q_push1(len > kSortMax, Lst.Q, make_seg(a, len, 0), st);
     } else if (len >= 2) {
         int i = atomicAdd(&st->nunits, 1);
         if (i < Lst.unit_cap) Lst.units[i] = make_item(a, len, kItemUnit, 0); else st->overflow = 1;
@@ -249,7 +308,7 @@ __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, un
     // merge-path passes with one output per thread
     for (int w = wid; w * 32 < NP; w += nw) {
         const int i = w * 32 + lane;
-        double x[1] = {i < P ? seg[i] : CUDART_INF};
+        double x[1] = {i < P ? __ldcg(seg + i) : CUDART_INF};
         warp_bitonic_sort<1>(x);
         W.sp[i] = x[0];
     }
@@ -854,67 +913,80 @@ struct EmitOut {
 };
 
 struct EmitArgs {
-    Seg *gnext;
+    Seg *gnext;        // next global level (> kLocalMax)
     int *ngnext;
     int gcap;
-    Seg *lnext;
-    int *nlnext;       // small local segments, stored from index 0 upwards
-    int *nlnext_big;   // big local segments (> kLocalBig), stored from index lcap-1 downwards
-    int lcap;
-    Seg *snext[kSortClasses];   // segment-sorter lists by size class
-    int *nsnext;                // counters nsnext[0..kSortClasses)
-    int scap[kSortClasses];
-    Item *units;
+    LeafQ Q;           // local / sort queues of the leaf kernel
+    Item *units;       // warp units (<= kUnitMax keys) and long fills
     int ucap;
-    int tag_round;     // pass / round number: makes unit tags unique per partition
-    double *keys;      // user buffer: short equality runs are written here directly
+    double *keys;      // user buffer: short equality runs and tiny gaps are written here directly
+    const double *tmp;
+    int in_leaf;       // emitting inside the leaf launch: local children go to the sort queue
 };
 
-// packed per-thread list counts for one block scan: units (<= 2 per thread,
-// 11 bits) and 0/1 list flags (10 bits each; blocks have <= 512 threads)
-constexpr int kPkU = 0, kPkL = 11, kPkLB = 21, kPkG = 31;
+// packed per-thread counts for one block scan (11 bits each; blocks <= 1024 threads):
+// units + fill items (<= 2 per thread), local items, global segments, sort items
+constexpr int kPkU = 0, kPkL = 11, kPkG = 22, kPkS = 33;
 __device__ __forceinline__ long long pk_get(long long x, int sh, int bits) { return (x >> sh) & ((1ll << bits) - 1); }
 
-__device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
-                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase, long long tag)
+// sort up to kTinyGap keys with one thread (src may equal dst)
+__device__ __forceinline__ void tiny_sort_copy(const double *src, double *dst, int m)
 {
-    // every equality run (class 2j+1) is final: it is written as a fill of the pivot value
-    int u_gap = 0, s_cls = -1, l_gap = 0, lb_gap = 0, g_gap = 0;
+    double a[kTinyGap];
+    for (int i = 0; i < m; ++i) {
+        const double x = src[i];
+        int j = i;
+        while (j > 0 && a[j - 1] > x) {
+            a[j] = a[j - 1];
+            --j;
+        }
+        a[j] = x;
+    }
+    for (int i = 0; i < m; ++i) dst[i] = a[i];
+}
+
+// Emission of one partition's classes, one pivot pair (gap 2j, run 2j+1) per thread:
+//  * gap <= kTinyGap                        -> sorted right here
+//  * kTinyGap < gap <= kUnitMax             -> warp unit
+//  * kUnitMax < gap <= kSortMax             -> sort queue
+//  * kSortMax < gap <= kLocalMax            -> local queue
+//  * gap > kLocalMax                        -> next global pass
+//  * equality run <= kFillDirect            -> written right here; longer -> fill item
+__device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
+                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase)
+{
+    int u_gap = 0, s_gap = 0, l_gap = 0, g_gap = 0, t_gap = 0;
     if (have && (gl >= 2 || (gl == 1 && dst_id == 1))) {
-        if (gl <= kUnitMax) u_gap = 1;
-        else if (gl <= kSortMax) s_cls = sort_class(gl);
-        else if (gl <= kLocalBig) l_gap = 1;
-        else if (gl <= kLocalMax) lb_gap = 1;
+        if (gl <= kTinyGap) {
+            tiny_sort_copy((dst_id ? A.tmp : A.keys) + ag, A.keys + ag, (int)gl);
+            t_gap = 1;
+        }
+        else if (gl <= kUnitMax) u_gap = 1;
+        else if (gl <= kSortMax) s_gap = 1;
+        else if (gl <= kLocalMax) l_gap = 1;
         else g_gap = 1;
     }
-    // equality runs: short ones are written right here, long ones become fill items
     if (have && el > 0 && el <= kFillDirect)
         for (long long i = 0; i < el; ++i) A.keys[ae + i] = pv;
     const int f_eq = (have && el > kFillDirect) ? 1 : 0;
     const int nu = u_gap + f_eq;
-    const long long pk = ((long long)nu << kPkU) | ((long long)l_gap << kPkL) | ((long long)lb_gap << kPkLB) |
-                         ((long long)g_gap << kPkG);
-    const long long pks = s_cls < 0 ? 0ll : (1ll << (20 * s_cls));   // sort classes: 20 bits each
-    long long tpk, tpks;
+    const long long pk = ((long long)nu << kPkU) | ((long long)l_gap << kPkL) | ((long long)g_gap << kPkG) |
+                         ((long long)s_gap << kPkS);
+    long long tpk;
     const long long xpk = block_exclusive_scan(pk, sh, &tpk);
-    const long long xpks = block_exclusive_scan(pks, sh, &tpks);
     if (threadIdx.x == 0) {
-        const int tu = (int)pk_get(tpk, kPkU, 11), tl = (int)pk_get(tpk, kPkL, 10);
-        const int tlb = (int)pk_get(tpk, kPkLB, 10), tg = (int)pk_get(tpk, kPkG, 10);
+        const int tu = (int)pk_get(tpk, kPkU, 11), tl = (int)pk_get(tpk, kPkL, 11);
+        const int tg = (int)pk_get(tpk, kPkG, 11), ts = (int)pk_get(tpk, kPkS, 11);
+        if (tl + ts) atomicAdd(&st->pending, tl + ts);   // before the slots become claimable
         sbase[0] = tu ? atomicAdd(&st->nunits, tu) : 0;
-        sbase[1] = tl ? atomicAdd(A.nlnext, tl) : 0;
+        sbase[1] = tl ? atomicAdd(A.in_leaf ? &st->sq_claim : &st->lq_claim, tl) : 0;
         sbase[2] = tg ? atomicAdd(A.ngnext, tg) : 0;
-        sbase[3] = tlb ? atomicAdd(A.nlnext_big, tlb) : 0;
-#pragma unroll
-        for (int c = 0; c < kSortClasses; ++c) {
-            const int ts = (int)pk_get(tpks, 20 * c, 20);
-            sbase[4 + c] = ts ? atomicAdd(&A.nsnext[c], ts) : 0;
-        }
+        sbase[3] = ts ? atomicAdd(&st->sq_claim, ts) : 0;
     }
     __syncthreads();
     long long ui = sbase[0] + pk_get(xpk, kPkU, 11);
     if (u_gap) {
-        if (ui < A.ucap) A.units[ui] = make_item(ag, gl, kItemUnit, dst_id, tag); else st->overflow = 3;
+        if (ui < A.ucap) A.units[ui] = make_item(ag, gl, kItemUnit, dst_id); else st->overflow = 3;
         ++ui;
     }
     if (f_eq) {
@@ -922,27 +994,22 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         it.value = pv;
         if (ui < A.ucap) A.units[ui] = it; else st->overflow = 3;
     }
-    if (s_cls >= 0) {   // static indexing of the argument arrays (no local-memory copy)
-        const long long i = sbase[4 + s_cls] + pk_get(xpks, 20 * s_cls, 20);
-        Seg *list = s_cls == 0 ? A.snext[0] : (s_cls == 1 ? A.snext[1] : A.snext[2]);
-        const int cap = s_cls == 0 ? A.scap[0] : (s_cls == 1 ? A.scap[1] : A.scap[2]);
-        if (i < cap) list[i] = make_seg(ag, gl, dst_id); else st->overflow = 5;
-    }
+    if (s_gap)
+        q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, (int)(sbase[3] + pk_get(xpk, kPkS, 11)),
+                  with_kind(make_seg(ag, gl, dst_id), kItemSort), A.Q.epoch);
     if (l_gap) {
-        const long long li = sbase[1] + pk_get(xpk, kPkL, 10);
-        if (li < A.lcap) A.lnext[li] = make_seg(ag, gl, dst_id); else st->overflow = 4;
-    }
-    if (lb_gap) {
-        const long long li = A.lcap - 1 - (sbase[3] + pk_get(xpk, kPkLB, 10));
-        if (li >= 0) A.lnext[li] = make_seg(ag, gl, dst_id); else st->overflow = 4;
+        const int i = (int)(sbase[1] + pk_get(xpk, kPkL, 11));
+        const Seg c = with_kind(make_seg(ag, gl, dst_id), kItemLocal);
+        if (A.in_leaf) q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, i, c, A.Q.epoch);
+        else q_publish(A.Q.lq, A.Q.lq_ready, A.Q.lcap, i, c, A.Q.epoch);
     }
     if (g_gap) {
-        const long long gi = sbase[2] + pk_get(xpk, kPkG, 10);
+        const long long gi = sbase[2] + pk_get(xpk, kPkG, 11);
         if (gi < A.gcap) A.gnext[gi] = make_seg(ag, gl, dst_id); else st->overflow = 4;
     }
     // keys in fills / units (block totals; segments < 2^31 keys)
     long long tk;
-    block_exclusive_scan((have ? el : 0) | ((u_gap ? gl : 0) << 32), sh, &tk);
+    block_exclusive_scan((have ? el : 0) | (((u_gap | t_gap) ? gl : 0) << 32), sh, &tk);
     EmitOut o;
     o.unit_keys = tk >> 32;
     o.fill_keys = tk & 0xffffffffll;
@@ -975,7 +1042,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
 {
     KS_PDL_ENTRY();
     __shared__ long long sh[33];
-    __shared__ long long sbase[4 + kSortClasses];
+    __shared__ long long sbase[4];
     if (abort_requested(st)) return;
     const int ns = *nseg;
     const int j0 = blockIdx.y * kPlanThreads;
@@ -997,8 +1064,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
                 pv = piv_pool[g.piv_off + j];
             }
         }
-        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase,
-                                     (g.start << 8) | (A.tag_round & 0xff));
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase);
         if (threadIdx.x == 0) {
             // keys of this chunk's classes [2 j0, 2 min(j0 + kPlanThreads, k + 1))
             const int jend = min(j0 + kPlanThreads, g.k + 1);
@@ -1022,102 +1088,89 @@ struct LocalSmem {
     unsigned hist[kRowsMaxLocal + 1];
     unsigned cursor[kRowsMaxLocal + 1];
     long long sh[33];
-    long long sbase[4 + kSortClasses];
-    int item;
+    long long sbase[4];
 };
 
-__global__ void __launch_bounds__(kLocalThreads) k_local(const Seg *lsegs, const int *nlocal, const int *nlocal_big,
-                                                         int lcap, EmitArgs A, DevStatus *st, double *keys,
-                                                         double *tmp)
+// Partition one local segment (in global memory, L2-resident) with its first
+// P keys, classes scattered into the other buffer, children emitted to the
+// queues (the same K-sort step as a global pass, by one CTA).  Loads bypass L1:
+// the segment may have been written by another SM during this launch.
+__device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStatus *st, double *keys,
+                          const double *tmp)
 {
-    KS_PDL_ENTRY();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    LocalSmem &L = *reinterpret_cast<LocalSmem *>(smem_raw);
-    if (abort_requested(st)) return;
-    const int nb = *nlocal_big, n = *nlocal + nb;
-    for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) L.item = atomicAdd(&st->local_next, 1);
-        __syncthreads();
-        const int d = L.item;
-        if (d >= n) break;
-        // big segments first (longest-processing-time order), from the top of the list
-        const Seg g = d < nb ? lsegs[lcap - 1 - d] : lsegs[d - nb];
-        const double *src = (g.src ? tmp : keys) + g.start;
-        double *dst = (g.src ? keys : tmp) + g.start;
-        const int dst_id = g.src ? 0 : 1;
-        const int m = (int)g.len;
-        const int P = pivots_for(m, kPMaxLocal);
-        int k, T;
-        double lo, scale;
-        KS_TR_DECL;
-        build_pivots(src, P, lut_for(P, kLutMaxLocal), L.piv, L.lut, L.W, k, T, lo, scale);
-        KS_TR(0);
-        const int rows = 2 * k + 1;
-        for (int c = threadIdx.x; c < rows; c += blockDim.x) L.hist[c] = 0;
-        __syncthreads();
-        constexpr int U = 8;
-        int i0 = 0;
-        for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
-            double v[U];
+    const double *src = (g.src ? tmp : keys) + g.start;
+    double *dst = (g.src ? keys : const_cast<double *>(tmp)) + g.start;
+    const int dst_id = g.src ? 0 : 1;
+    const int m = (int)g.len;
+    const int P = pivots_for(m, kPMaxLocal);
+    int k, T;
+    double lo, scale;
+    KS_TR_DECL;
+    build_pivots(src, P, lut_for(P, kLutMaxLocal), L.piv, L.lut, L.W, k, T, lo, scale);
+    KS_TR(0);
+    const int rows = 2 * k + 1;
+    for (int c = threadIdx.x; c < rows; c += blockDim.x) L.hist[c] = 0;
+    __syncthreads();
+    constexpr int U = 8;
+    int i0 = 0;
+    for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
+        double v[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = src[i0 + u * kLocalThreads + threadIdx.x];
+        for (int u = 0; u < U; ++u) v[u] = __ldcg(src + i0 + u * kLocalThreads + threadIdx.x);
 #pragma unroll
-            for (int u = 0; u < U; ++u) atomicAdd(&L.hist[classify(v[u], L.piv, L.lut, lo, scale, T)], 1u);
-        }
-        for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads)
-            atomicAdd(&L.hist[classify(src[i], L.piv, L.lut, lo, scale, T)], 1u);
-        __syncthreads();
-        KS_TR(1);
-        {   // exclusive scan of the class histogram -> class starts (2 classes per thread)
-            const int c0 = 2 * threadIdx.x;
-            const unsigned h0 = c0 < rows ? L.hist[c0] : 0u;
-            const unsigned h1 = c0 + 1 < rows ? L.hist[c0 + 1] : 0u;
-            const long long ex = block_exclusive_scan((long long)h0 + h1, L.sh, nullptr);
-            if (c0 < rows) L.cursor[c0] = (unsigned)ex;
-            if (c0 + 1 < rows) L.cursor[c0 + 1] = (unsigned)ex + h0;
-        }
-        __syncthreads();
-        i0 = 0;
-        for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
-            double v[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) v[u] = src[i0 + u * kLocalThreads + threadIdx.x];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int c = classify(v[u], L.piv, L.lut, lo, scale, T);
-                if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v[u];
-            }
-        }
-        for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads) {
-            const double v = src[i];
-            const int c = classify(v, L.piv, L.lut, lo, scale, T);
-            if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v;
-        }
-        __syncthreads();
-        KS_TR(2);
-        // class starts = cursor - (keys written); emit per pivot pair
-        const int j = threadIdx.x;
-        const bool have = j <= k;
-        long long ag = 0, gl = 0, ae = 0, el = 0;
-        double pv = 0.0;
-        if (have) {
-            gl = L.hist[2 * j];
-            ag = (long long)L.cursor[2 * j] - gl;
-            if (j < k) {
-                el = L.hist[2 * j + 1];
-                ae = (long long)L.cursor[2 * j + 1];   // equality runs are not scattered: cursor = start
-                pv = L.piv[j];
-            }
-        }
-        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase,
-                                     (g.start << 8) | (A.tag_round & 0xff));
-        if (threadIdx.x == 0) account_partition(st, g.len, o, true);
-        KS_TR(3);
-#ifdef KS_TRACE
-        if (threadIdx.x == 0) { atomicAdd(&g_trace[4], 1ull); atomicAdd(&g_trace[5], (unsigned long long)m); }
-#endif
+        for (int u = 0; u < U; ++u) atomicAdd(&L.hist[classify(v[u], L.piv, L.lut, lo, scale, T)], 1u);
     }
+    for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads)
+        atomicAdd(&L.hist[classify(__ldcg(src + i), L.piv, L.lut, lo, scale, T)], 1u);
+    __syncthreads();
+    KS_TR(1);
+    {   // exclusive scan of the class histogram -> class starts (2 classes per thread)
+        const int c0 = 2 * threadIdx.x;
+        const unsigned h0 = c0 < rows ? L.hist[c0] : 0u;
+        const unsigned h1 = c0 + 1 < rows ? L.hist[c0 + 1] : 0u;
+        const long long ex = block_exclusive_scan((long long)h0 + h1, L.sh, nullptr);
+        if (c0 < rows) L.cursor[c0] = (unsigned)ex;
+        if (c0 + 1 < rows) L.cursor[c0 + 1] = (unsigned)ex + h0;
+    }
+    __syncthreads();
+    i0 = 0;
+    for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcg(src + i0 + u * kLocalThreads + threadIdx.x);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int c = classify(v[u], L.piv, L.lut, lo, scale, T);
+            if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v[u];
+        }
+    }
+    for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads) {
+        const double v = __ldcg(src + i);
+        const int c = classify(v, L.piv, L.lut, lo, scale, T);
+        if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v;
+    }
+    __syncthreads();
+    KS_TR(2);
+    // class starts = cursor - (keys written); emit per pivot pair
+    const int j = threadIdx.x;
+    const bool have = j <= k;
+    long long ag = 0, gl = 0, ae = 0, el = 0;
+    double pv = 0.0;
+    if (have) {
+        gl = L.hist[2 * j];
+        ag = (long long)L.cursor[2 * j] - gl;
+        if (j < k) {
+            el = L.hist[2 * j + 1];
+            ae = (long long)L.cursor[2 * j + 1];   // equality runs are not scattered: cursor = start
+            pv = L.piv[j];
+        }
+    }
+    const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase);
+    if (threadIdx.x == 0) account_partition(st, g.len, o, true);
+    KS_TR(3);
+#ifdef KS_TRACE
+    if (threadIdx.x == 0) { atomicAdd(&g_trace[4], 1ull); atomicAdd(&g_trace[5], (unsigned long long)m); }
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1287,81 +1340,59 @@ __device__ __noinline__ bool warp_sort_bucket(double *a, int sz)
     return true;
 }
 
-// One size class of the segment sorter: entries list[d] for d < *count,
-// pulled from a work counter; thread 0 prefetches the next descriptor while
-// the block works on the current one.  The per-segment code path is kept
-// short (no unrolled remainders): segments hold only ~10 keys per thread.
+// Sort one segment (kUnitMax < len <= kSortMax) on chip and write it to its
+// final place in the user buffer (see the segment-sorter notes above).
 template <int C>
-__global__ void __launch_bounds__(sort_threads(C),
-                                  sort_threads(C) >= 1024 ? 1 : (sort_threads(C) >= 512 ? 2 : (sort_threads(C) >= 256 ? 3 : 5)))
-    k_segsort(const Seg *list, const int *count, int *next, Seg *lnext, int *nlnext, int lcap, DevStatus *st,
-              double *keys, const double *tmp)
+__device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevStatus *st, double *keys,
+                            const double *tmp)
 {
-    KS_PDL_ENTRY();
     using Smem = SortSmem<C>;
     constexpr int kT = Smem::kT;
     constexpr int kWarps = kT / 32;
     static_assert(Smem::kPB * kT == Smem::kBuckets, "whole buckets per thread");
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem &S = *reinterpret_cast<Smem *>(smem_raw);
-    if (abort_requested(st)) return;
-    const int n = *count;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    if (tid == 0) {
-        const int d = atomicAdd(next, 1);
-        S.item = d;
-        S.nbig = 0;
-        if (d < n) {
-            const Seg g = list[d];
-            S.start = g.start;
-            S.len = (int)g.len;
-            S.src = g.src;
-#if KS_PREFETCH
-            l2_prefetch(keys + g.start, 8ull * g.len);
-#endif
+    const long long start = g.start;
+    const int m = (int)g.len;
+    const double *in = (g.src ? tmp : keys) + start;
+    double *out = keys + start;
+    // 1. load (coalesced, 4 loads in flight per thread, L2 only) + min / max
+    double mn = CUDART_INF, mx = -CUDART_INF;
+    for (int i0 = 0; i0 < m; i0 += 4 * kT) {
+        double x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kT + tid;
+            x[u] = i < m ? __ldcg(in + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = i0 + u * kT + tid;
+            if (i < m) {
+                S.a[i] = x[u];
+                mn = x[u] < mn ? x[u] : mn;
+                mx = x[u] > mx ? x[u] : mx;
+            }
         }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
+        mn = p < mn ? p : mn;
+        mx = q > mx ? q : mx;
+    }
+    if (lane == 0) {
+        S.red[0][wid] = mn;
+        S.red[1][wid] = mx;
+    }
+    int B = m / Smem::kLam;
+    B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
+#pragma unroll 1
+    for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
+    if (tid == 0) S.nbig = 0;
     __syncthreads();
-    unsigned long long keys_done = 0, segs_done = 0;
-    for (;;) {
-        if (S.item >= n) break;
-        const long long start = S.start;
-        const int m = S.len;
-        const double *in = (S.src ? tmp : keys) + start;
-        double *out = keys + start;
-        const bool copy_const = S.src != 0;
-        // thread 0: claim and load the next descriptor (lands in smem at the end)
-        int nd = 0;
-        long long nstart = 0;
-        int nlen = 0, nsrc = 0;
-        if (tid == 0) {
-            nd = atomicAdd(next, 1);
-            if (nd < n) {
-                const Seg g = list[nd];
-                nstart = g.start;
-                nlen = (int)g.len;
-                nsrc = g.src;
-            }
-        }
-        // 1. load (coalesced, 4 loads in flight per thread) + min / max
-        double mn = CUDART_INF, mx = -CUDART_INF;
-        for (int i0 = 0; i0 < m; i0 += 4 * kT) {
-            double x[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + u * kT + tid;
-                x[u] = i < m ? in[i] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int i = i0 + u * kT + tid;
-                if (i < m) {
-                    S.a[i] = x[u];
-                    mn = x[u] < mn ? x[u] : mn;
-                    mx = x[u] > mx ? x[u] : mx;
-                }
-            }
-        }
+    if (wid == 0) {   // block min / max and the bucket scale, broadcast through shared memory
+        mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
+        mx = lane < kWarps ? S.red[1][lane] : -CUDART_INF;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
@@ -1369,133 +1400,185 @@ __global__ void __launch_bounds__(sort_threads(C),
             mx = q > mx ? q : mx;
         }
         if (lane == 0) {
-            S.red[0][wid] = mn;
-            S.red[1][wid] = mx;
+            double scale = mx > mn ? (double)B / (mx - mn) : -1.0;            // -1: constant segment
+            if (mx > mn && (!(scale > 0.0) || isinf(scale))) scale = 0.0;    // range overflow / underflow
+            S.bounds[0] = mn;
+            S.bounds[1] = scale;
         }
-        int B = m / Smem::kLam;
-        B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
-#pragma unroll 1
-        for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
-        __syncthreads();
-        if (wid == 0) {   // block min / max and the bucket scale, broadcast through shared memory
-            mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
-            mx = lane < kWarps ? S.red[1][lane] : -CUDART_INF;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
-                mn = p < mn ? p : mn;
-                mx = q > mx ? q : mx;
-            }
-            if (lane == 0) {
-                double scale = mx > mn ? (double)B / (mx - mn) : -1.0;            // -1: constant segment
-                if (mx > mn && (!(scale > 0.0) || isinf(scale))) scale = 0.0;    // range overflow / underflow
-                S.bounds[0] = mn;
-                S.bounds[1] = scale;
-            }
-        }
-        __syncthreads();
-        const double lo = S.bounds[0];
-        const double scale = S.bounds[1];
-        if (scale < 0.0) {   // constant segment: already sorted
-            if (copy_const) {
-#pragma unroll 1
-                for (int i = tid; i < m; i += kT) out[i] = S.a[i];
-            }
-        } else {
-            if (scale == 0.0) B = 1;   // one bucket: the warp path (or the partitioner) takes it
-            // 2. bucket histogram, scan, scatter a -> b
-#pragma unroll 1
-            for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[sort_bucket(S.a[i], lo, scale, B)], 1u);
-            __syncthreads();
-            {
-                const int b0 = tid * Smem::kPB;
-                unsigned c[Smem::kPB];
-                unsigned t = 0;
-#pragma unroll
-                for (int e = 0; e < Smem::kPB; ++e) {
-                    c[e] = b0 + e < B ? S.cur[b0 + e] : 0u;
-                    t += c[e];
-                }
-                unsigned ex = block_exclusive_scan_u32(t, S.sh, nullptr);
-                unsigned bigmask = 0;
-#pragma unroll
-                for (int e = 0; e < Smem::kPB; ++e) {
-                    if (b0 + e < B) S.cur[b0 + e] = ex;
-                    ex += c[e];
-                    bigmask |= (c[e] > (unsigned)kThreadSortMax ? 1u : 0u) << e;
-                }
-                while (bigmask) {   // rare: buckets for the warp path
-                    const int e = __ffs(bigmask) - 1;
-                    bigmask &= bigmask - 1;
-                    S.big[atomicAdd(&S.nbig, 1)] = b0 + e;
-                }
-            }
-            __syncthreads();
-#pragma unroll 1
-            for (int i = tid; i < m; i += kT) {
-                const double x = S.a[i];
-                S.b[atomicAdd(&S.cur[sort_bucket(x, lo, scale, B)], 1u)] = x;
-            }
-            __syncthreads();
-            // 3. cur[b] is now the end of bucket b.  Buckets of more than
-            //    kThreadSortMax keys (listed by the scan; none for smooth
-            //    inputs) are sorted in place by one warp each.
-            const int nbig = S.nbig;
-            if (nbig) {
-                for (int q = wid; q < nbig; q += kWarps) {
-                    const int b = S.big[q];
-                    const int s0 = b ? (int)S.cur[b - 1] : 0;
-                    const int sz = (int)S.cur[b] - s0;
-                    if (!warp_sort_bucket(S.b + s0, sz) && lane == 0) {   // skewed: back to the first-key partitioner
-                        const int li = atomicAdd(nlnext, 1);
-                        if (li < lcap) lnext[li] = make_seg(start + s0, sz, 0); else st->overflow = 6;
-                    }
-                }
-                __syncthreads();
-            }
-            // 4. every key of a small bucket takes its rank inside the bucket
-            //    (ties by position: equal keys are bitwise equal here) and is
-            //    written straight to its final place
-#pragma unroll 1
-            for (int i = tid; i < m; i += kT) {
-                const double x = S.b[i];
-                const int bk = sort_bucket(x, lo, scale, B);
-                const int e = (int)S.cur[bk];
-                const int s0 = bk ? (int)S.cur[bk - 1] : 0;
-                int pos = i;
-                if (e - s0 > 1 && e - s0 <= kThreadSortMax) {
-                    int r = s0;
-#pragma unroll 1
-                    for (int j = s0; j < e; ++j) {
-                        const double y = S.b[j];
-                        r += (y < x || (y == x && j < i)) ? 1 : 0;
-                    }
-                    pos = r;
-                }
-                out[pos] = x;
-            }
-        }
-        keys_done += (unsigned long long)m;
-        segs_done += 1;
-        if (tid == 0) {
-            S.item = nd;
-            S.start = nstart;
-            S.len = nlen;
-            S.src = nsrc;
-            S.nbig = 0;
-#if KS_PREFETCH
-            if (nd < n) {   // next segment: its input and (when different) its output range
-                l2_prefetch((nsrc ? tmp : keys) + nstart, 8ull * nlen);
-                if (nsrc) l2_prefetch(keys + nstart, 8ull * nlen);
-            }
-#endif
-        }
-        __syncthreads();
     }
-    if (tid == 0 && segs_done) {
-        add_bytes(st, kPhLeaf, 16ull * keys_done);
-        atomicAdd(&st->keys_leaf, keys_done);
-        atomicAdd(&st->leaves, segs_done);
+    __syncthreads();
+    const double lo = S.bounds[0];
+    const double scale = S.bounds[1];
+    if (scale < 0.0) {   // constant segment: already sorted
+        if (g.src) {
+#pragma unroll 1
+            for (int i = tid; i < m; i += kT) out[i] = S.a[i];
+        }
+    } else {
+        if (scale == 0.0) B = 1;   // one bucket: the warp path (or the partitioner) takes it
+        // 2. bucket histogram, scan, scatter a -> b
+#pragma unroll 1
+        for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[sort_bucket(S.a[i], lo, scale, B)], 1u);
+        __syncthreads();
+        {
+            const int b0 = tid * Smem::kPB;
+            unsigned c[Smem::kPB];
+            unsigned t = 0;
+#pragma unroll
+            for (int e = 0; e < Smem::kPB; ++e) {
+                c[e] = b0 + e < B ? S.cur[b0 + e] : 0u;
+                t += c[e];
+            }
+            unsigned ex = block_exclusive_scan_u32(t, S.sh, nullptr);
+            unsigned bigmask = 0;
+#pragma unroll
+            for (int e = 0; e < Smem::kPB; ++e) {
+                if (b0 + e < B) S.cur[b0 + e] = ex;
+                ex += c[e];
+                bigmask |= (c[e] > (unsigned)kThreadSortMax ? 1u : 0u) << e;
+            }
+            while (bigmask) {   // rare: buckets for the warp path
+                const int e = __ffs(bigmask) - 1;
+                bigmask &= bigmask - 1;
+                S.big[atomicAdd(&S.nbig, 1)] = b0 + e;
+            }
+        }
+        __syncthreads();
+#pragma unroll 1
+        for (int i = tid; i < m; i += kT) {
+            const double x = S.a[i];
+            S.b[atomicAdd(&S.cur[sort_bucket(x, lo, scale, B)], 1u)] = x;
+        }
+        __syncthreads();
+        // 3. cur[b] is now the end of bucket b.  Buckets of more than
+        //    kThreadSortMax keys (listed by the scan; none for smooth
+        //    inputs) are sorted in place by one warp each.
+        const int nbig = S.nbig;
+        if (nbig) {
+            for (int q = wid; q < nbig; q += kWarps) {
+                const int b = S.big[q];
+                const int s0 = b ? (int)S.cur[b - 1] : 0;
+                const int sz = (int)S.cur[b] - s0;
+                if (!warp_sort_bucket(S.b + s0, sz) && lane == 0)   // skewed: back to the first-key partitioner
+                    q_push1(true, Q, make_seg(start + s0, sz, 0), st);
+            }
+            __syncthreads();
+        }
+        // 4. every key of a small bucket takes its rank inside the bucket
+        //    (ties by position: equal keys are bitwise equal here) and is
+        //    written straight to its final place
+#pragma unroll 1
+        for (int i = tid; i < m; i += kT) {
+            const double x = S.b[i];
+            const int bk = sort_bucket(x, lo, scale, B);
+            const int e = (int)S.cur[bk];
+            const int s0 = bk ? (int)S.cur[bk - 1] : 0;
+            int pos = i;
+            if (e - s0 > 1 && e - s0 <= kThreadSortMax) {
+                int r = s0;
+#pragma unroll 1
+                for (int j = s0; j < e; ++j) {
+                    const double y = S.b[j];
+                    r += (y < x || (y == x && j < i)) ? 1 : 0;
+                }
+                pos = r;
+            }
+            out[pos] = x;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// leaf kernel: one persistent CTA per SM drains the local queue (biggest work
+// first: each local partition feeds the sort queue) and then the sort queue,
+// in one launch -- the long local partitions overlap the segment sorts, and
+// the segment sorter's hand-backs are picked up without a host round trip.
+// The launch ends when no item is queued or running.
+// ---------------------------------------------------------------------------
+constexpr int kLeafThreads = 1024;
+static_assert(kLocalThreads == kLeafThreads, "the local partitioner runs inside the leaf kernel");
+static_assert(sort_threads(2) == kLeafThreads, "the segment sorter runs inside the leaf kernel");
+
+struct LeafCtl {
+    Seg seg;
+    int kind;   // -1 done, 0 local partition, 1 segment sort
+};
+constexpr size_t kLeafSmem =
+    (sizeof(SortSmem<2>) > sizeof(LocalSmem) ? sizeof(SortSmem<2>) : sizeof(LocalSmem)) + sizeof(LeafCtl) + 64;
+
+__global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus *st, double *keys,
+                                                         const double *tmp)
+{
+    KS_PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    LeafCtl &ctl = *reinterpret_cast<LeafCtl *>(smem_raw + (kLeafSmem - sizeof(LeafCtl) - 64));
+    if (abort_requested(st)) return;
+    const LeafQ &Q = A.Q;
+    unsigned long long keys_sorted = 0, segs_sorted = 0;
+#ifdef KS_TRACE
+    long long tr_t0 = clock64();
+#endif
+    // the plan's local items (all published before this launch): a fixed set
+    const int lq_n = *reinterpret_cast<volatile int *>(&st->lq_claim);
+    bool local_phase = true;   // (thread 0 only)
+    for (;;) {
+        if (threadIdx.x == 0) {
+            int kind = -1;
+            // 1. the plan's local partitions, biggest work first: one ticket each
+            if (local_phase) {
+                const int idx = atomicAdd(&st->lq_head, 1);
+                if (idx < lq_n) {
+                    const int slot = idx % Q.lcap;
+                    while (ld_acquire_u64(&Q.lq_ready[slot]) != q_tag(Q.epoch, idx)) __nanosleep(32);
+                    const Seg *q = Q.lq + slot;
+                    ctl.seg = make_seg(__ldcg(&q->start), __ldcg(&q->len), __ldcg(&q->src));
+                    kind = kItemLocal;
+                } else {
+                    local_phase = false;
+                }
+            }
+            // 2. the sort queue: take a ticket, wait until it is published or no work is left
+            if (kind < 0) {
+                const int idx = atomicAdd(&st->sq_head, 1);
+                for (;;) {
+                    if (idx < ld_acquire_s32(&st->sq_claim)) {
+                        const int slot = idx % Q.scap;
+                        while (ld_acquire_u64(&Q.sq_ready[slot]) != q_tag(Q.epoch, idx)) __nanosleep(32);
+                        const Seg *q = Q.sq + slot;
+                        ctl.seg = make_seg(__ldcg(&q->start), __ldcg(&q->len), __ldcg(&q->src));
+                        kind = __ldcg(&q->k);
+                        break;
+                    }
+                    if (ld_acquire_s32(&st->pending) == 0) break;   // nothing queued or running: done
+                    __nanosleep(128);
+                }
+            }
+            ctl.kind = kind;
+        }
+        __syncthreads();
+        KS_TR(13);   // item fetch (incl. waiting for work)
+        const int kind = ctl.kind;
+        if (kind < 0) break;
+        const Seg g = ctl.seg;
+        if (kind == kItemLocal) {
+            local_one(*reinterpret_cast<LocalSmem *>(smem_raw), g, A, st, keys, tmp);
+            KS_TR(14);
+        } else {
+            segsort_one<2>(*reinterpret_cast<SortSmem<2> *>(smem_raw), g, Q, st, keys, tmp);
+            keys_sorted += (unsigned long long)g.len;
+            segs_sorted += 1;
+            KS_TR(15);
+        }
+        __syncthreads();   // this item's children are published; smem free for the next one
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicSub(&st->pending, 1);
+        }
+    }
+    if (threadIdx.x == 0 && segs_sorted) {
+        add_bytes(st, kPhLeaf, 16ull * keys_sorted);
+        atomicAdd(&st->keys_leaf, keys_sorted);
+        atomicAdd(&st->leaves, segs_sorted);
     }
 }
 
@@ -1615,29 +1698,25 @@ FastLayout fast_layout(long long n, long long nseg0)
     FastLayout L{};
     L.n = n;
     L.seg_cap = (int)(n / (kLocalMax + 1) + 2);                  // global-pass segments
-    L.lseg_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);          // local-partition segments per round
-    for (int c = 0; c < kSortClasses; ++c)                       // segment-sorter lists (disjoint ranges)
-        L.sseg_cap[c] = (int)(n / ((c ? sort_cap(c - 1) : kUnitMax) + 1) + nseg0 + 2);
+    // leaf queues: queued items are disjoint ranges of > kUnitMax keys, plus CTAs in flight
+    L.lq_cap = (int)(n / (kUnitMax + 1) + nseg0 + 4096);
+    L.sq_cap = L.lq_cap;
     const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
     L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
     L.mat_cap = (2 * psum + L.seg_cap) + (long long)(2 * kPMax + 1) * (2 * (n / kChunk) + 2);
-    // finishing items emitted by one round <= 2 per pivot + 1 per segment; later the list
-    // is flushed whenever it is more than half full
-    // (the speculative schedule runs up to four partition rounds before the first flush)
-    L.unit_cap = (int)(4 * (2 * (n / kKeysPerPivot) + 3 * (long long)L.lseg_cap + 2 * L.seg_cap) + 4096);
+    // warp units and fill items of one leaf launch: disjoint final ranges of > kTinyGap keys
+    L.unit_cap = (int)(2 * (n / (kTinyGap + 1)) + nseg0 + 4096);
     L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
     size_t off = 0;
     L.o_status = off; off = align_up(off + sizeof(DevStatus));
     L.o_seg[0] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
     L.o_seg[1] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
-    L.o_lseg[0] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
-    L.o_lseg[1] = off; off = align_up(off + sizeof(Seg) * L.lseg_cap);
-    for (int c = 0; c < kSortClasses; ++c) {
-        L.o_sseg[c] = off;
-        off = align_up(off + sizeof(Seg) * L.sseg_cap[c]);
-    }
+    L.o_lq_ready = off; off = align_up(off + sizeof(unsigned long long) * L.lq_cap);   // (ready words contiguous:
+    L.o_sq_ready = off; off = align_up(off + sizeof(unsigned long long) * L.sq_cap);   //  one clear per call)
+    L.o_lq = off; off = align_up(off + sizeof(Seg) * L.lq_cap);
+    L.o_sq = off; off = align_up(off + sizeof(Seg) * L.sq_cap);
     L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
     L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
     L.o_lut = off; off = align_up(off + sizeof(unsigned) * L.lut_cap);
@@ -1653,7 +1732,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 // Per-device launch shapes and kernel attributes, set up once per process
 // (cudaFuncSetAttribute / occupancy queries cost host time on every call).
 struct EngineCfg {
-    int sms, g_count, g_scatter, g_units, g_local, g_sortc[kSortClasses];
+    int sms, g_count, g_scatter, g_units, g_leaf;
 };
 
 static const EngineCfg *engine_cfg()
@@ -1671,13 +1750,10 @@ static const EngineCfg *engine_cfg()
         ok = ok && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) == cudaSuccess;
     };
     smem(k_scatter, sizeof(ScatterSmem));
-    smem(k_local, sizeof(LocalSmem));
     smem(k_pivots, sizeof(PivotsSmem));
     smem(k_count<true>, sizeof(CountSmem));
     smem(k_count<false>, sizeof(CountSmem));
-    smem(k_segsort<0>, sizeof(SortSmem<0>));
-    smem(k_segsort<1>, sizeof(SortSmem<1>));
-    smem(k_segsort<2>, sizeof(SortSmem<2>));
+    smem(k_leaf, kLeafSmem);
     if (!ok) {
         fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
         return nullptr;
@@ -1691,10 +1767,7 @@ static const EngineCfg *engine_cfg()
     c.g_count = grid(k_count<false>, kCountThreads, sizeof(CountSmem));
     c.g_scatter = grid(k_scatter, kPassThreads, sizeof(ScatterSmem));
     c.g_units = grid(k_finish_units, kUnitWarps * 32, 0);
-    c.g_local = grid(k_local, kLocalThreads, sizeof(LocalSmem));
-    c.g_sortc[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
-    c.g_sortc[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
-    c.g_sortc[2] = grid(k_segsort<2>, sort_threads(2), sizeof(SortSmem<2>));
+    c.g_leaf = grid(k_leaf, kLeafThreads, kLeafSmem);
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -1708,9 +1781,6 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     char *w = static_cast<char *>(ws);
     DevStatus *st = reinterpret_cast<DevStatus *>(w + L.o_status);
     Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.o_seg[0]), reinterpret_cast<Seg *>(w + L.o_seg[1])};
-    Seg *lsegs[2] = {reinterpret_cast<Seg *>(w + L.o_lseg[0]), reinterpret_cast<Seg *>(w + L.o_lseg[1])};
-    Seg *ssegs[kSortClasses];
-    for (int c = 0; c < kSortClasses; ++c) ssegs[c] = reinterpret_cast<Seg *>(w + L.o_sseg[c]);
     int *chunk_seg = reinterpret_cast<int *>(w + L.o_chunk);
     double *piv = reinterpret_cast<double *>(w + L.o_piv);
     unsigned *lut = reinterpret_cast<unsigned *>(w + L.o_lut);
@@ -1719,12 +1789,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     long long *bsum = reinterpret_cast<long long *>(w + L.o_bsum);
     Item *units = reinterpret_cast<Item *>(w + L.o_units);
     double *tmp = reinterpret_cast<double *>(w + L.o_tmp);
+    LeafQ Q{reinterpret_cast<Seg *>(w + L.o_lq), reinterpret_cast<unsigned long long *>(w + L.o_lq_ready), L.lq_cap,
+            reinterpret_cast<Seg *>(w + L.o_sq), reinterpret_cast<unsigned long long *>(w + L.o_sq_ready), L.sq_cap,
+            1};
 
     const EngineCfg *cfg = engine_cfg();
     if (cfg == nullptr) return KS_CUDA_ERROR;
     const int sms = cfg->sms;
-    const int g_count = cfg->g_count, g_scatter = cfg->g_scatter, g_units = cfg->g_units, g_local = cfg->g_local;
-    const int *g_sortc = cfg->g_sortc;
+    const int g_count = cfg->g_count, g_scatter = cfg->g_scatter, g_units = cfg->g_units, g_leaf = cfg->g_leaf;
     const int g_scan = sms * 2;
     const int g_pivots = sms;
     Launcher K(stream, profile);
@@ -1737,31 +1809,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         return h.overflow ? KS_CUDA_ERROR : KS_OK;
     };
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
-    int lc = 0;
-    auto flush_units = [&]() {
-        // segment sorter first: its rare hand-backs go to the current local list
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->sort_next[0], &st->sort_next[1], &st->sort_next[2],
-               (int *)nullptr);
-        // largest class first: its CTAs hold a whole SM each
-        K.run(kPhLeaf, [&] {
-            launch(k_segsort<2>, dim3(g_sortc[2]), dim3(sort_threads(2)), sizeof(SortSmem<2>), stream, ssegs[2], &st->nsort[2], &st->sort_next[2], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
-        });
-        K.run(kPhLeaf, [&] {
-            launch(k_segsort<1>, dim3(g_sortc[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, ssegs[1], &st->nsort[1], &st->sort_next[1], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
-        });
-        K.run(kPhLeaf, [&] {
-            launch(k_segsort<0>, dim3(g_sortc[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, ssegs[0], &st->nsort[0], &st->sort_next[0], lsegs[lc], &st->nlocal[lc], L.lseg_cap, st, keys, tmp);
-        });
-        K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nsort[0], &st->nsort[1], &st->nsort[2], &st->nunits);
-    };
 
+    // queue ready words: cleared once per call (their tags carry the leaf epoch)
+    KS_CK(cudaMemsetAsync(Q.lq_ready, 0, L.o_lq - L.o_lq_ready, stream));
     if (d_off != nullptr) {   // (the single-array init kernel clears the status itself)
         KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
         KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
     }
-    const InitLists Lst{segs[0], lsegs[0], {ssegs[0], ssegs[1], ssegs[2]}, units, L.seg_cap, L.lseg_cap,
-                        {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]}, L.unit_cap};
+    const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
     if (d_off == nullptr) {
         K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
         if (n <= kLocalMax)
@@ -1772,11 +1827,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     }
 
     // The schedule is launched speculatively without host round-trips: global
-    // passes and local rounds read their work counts on the device and exit
-    // at once when empty.  One status read at the end; inputs that need more
-    // passes (adversarial shapes: presorted, few distinct values, ...) continue
-    // in a synchronising loop.
-    int level = 0, gcur = 0, rounds = 0;
+    // passes read their segment counts on the device (and exit at once when
+    // empty), the leaf kernel drains its queues by itself.  One status read at
+    // the end; inputs that need more global passes (adversarial shapes:
+    // presorted, few distinct values, ...) continue in a synchronising loop.
+    int level = 0, gcur = 0, leaves_run = 0;
     auto global_pass = [&]() {
         const double *src = (level & 1) ? tmp : keys;
         double *dst = (level & 1) ? keys : tmp;
@@ -1786,22 +1841,24 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
         const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
-        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap,
-                   {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
-                   units, L.unit_cap, level, keys};
+        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0};
         K.run(kPhPivots, [&] {
-            launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap, L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next);
+            launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
+                   L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next);
         });
         K.run(kPhPivots, [&] {
-            launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src, piv, lut, chunk_seg);
+            launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src, piv,
+                   lut, chunk_seg);
         });
         if (level == 0)
             K.run(kPhCount, [&] {
-                launch(k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
+                launch(k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
+                       chunk_seg, st, src, piv, lut, mat, st);
             });
         else
             K.run(kPhCount, [&] {
-                launch(k_count<false>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur], chunk_seg, st, src, piv, lut, mat, st);
+                launch(k_count<false>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
+                       chunk_seg, st, src, piv, lut, mat, st);
             });
 #if KS_SCAN3
         K.run(kPhScan, [&] { launch(k_scan_reduce, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st, bsum); });
@@ -1809,49 +1866,42 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         K.run(kPhScan, [&] { launch(k_scan_apply, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st, bsum, moff); });
 #else
         K.run(kPhScan, [&] {
-            launch(k_scan_lookback, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st, reinterpret_cast<unsigned long long *>(bsum), moff);
+            launch(k_scan_lookback, dim3(g_scan), dim3(kScanThreads), 0, stream, mat, st,
+                   reinterpret_cast<unsigned long long *>(bsum), moff);
         });
 #endif
         K.run(kPhScatter, [&] {
-            launch(k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur], chunk_seg, st, src, dst, piv, lut, moff, mat);
+            launch(k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur], chunk_seg,
+                   st, src, dst, piv, lut, moff, mat);
         });
         K.run(kPhPlan, [&] {
-            launch(k_plan, dim3(dim3(gx, kPlanChunks)), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A, st, dst_id);
+            launch(k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A,
+                   st, dst_id);
         });
         ++level;
         gcur ^= 1;
     };
-    auto local_round = [&]() {
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->local_next, &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
-               (int *)nullptr);
-        EmitArgs A{segs[gcur], &st->nseg[gcur], 0, lsegs[lc ^ 1], &st->nlocal[lc ^ 1], &st->nlocal_big[lc ^ 1],
-                   L.lseg_cap, {ssegs[0], ssegs[1], ssegs[2]}, st->nsort, {L.sseg_cap[0], L.sseg_cap[1], L.sseg_cap[2]},
-                   units, L.unit_cap, 128 + rounds, keys};
-        K.run(kPhOther, [&] {
-            launch(k_local, dim3(g_local), dim3(kLocalThreads), sizeof(LocalSmem), stream, lsegs[lc], &st->nlocal[lc], &st->nlocal_big[lc], L.lseg_cap, A, st, keys, tmp);
-        });
-        lc ^= 1;
-        ++rounds;
+    // leaf launch: queues -> sorted ranges, then the warp units and fills
+    auto leaf = [&]() {
+        EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1};
+        K.run(kPhLeaf, [&] { launch(k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head);
+        K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nunits, (int *)nullptr, (int *)nullptr, (int *)nullptr);
+        ++Q.epoch;
+        ++leaves_run;
     };
-    // speculative part: expected shape of a random input
-    const int spec_global = n > kLocalMax ? 1 : 0;
-    for (int i = 0; i < spec_global; ++i) global_pass();
-    local_round();
-    local_round();
-    flush_units();
+    if (n > kLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
+    leaf();
     int rc = sync_status();
     if (rc != KS_OK) return rc;
-    // remaining work (rare): finish with host checks
-    while (!aborted() &&
-           (h.nseg[gcur] > 0 || h.nlocal[lc] + h.nlocal_big[lc] > 0 || h.nunits > 0 ||
-            h.nsort[0] + h.nsort[1] + h.nsort[2] > 0)) {
-        if (h.nseg[gcur] > 0) global_pass();
-        else if (h.nlocal[lc] + h.nlocal_big[lc] > 0) local_round();
-        if (h.nunits > L.unit_cap / 2 || (h.nseg[gcur] == 0 && h.nlocal[lc] + h.nlocal_big[lc] == 0)) flush_units();
+    while (!aborted() && h.nseg[gcur] > 0) {   // remaining work (rare): more global levels
+        global_pass();
+        leaf();
         rc = sync_status();
         if (rc != KS_OK) return rc;
     }
-    res->levels = level + rounds;
+    res->levels = level + leaves_run;
     res->bad_index = h.bad_index == kNoIndex ? -1 : (long long)h.bad_index;
     res->mixed_zero = (h.pos_zero && h.neg_zero) ? 1 : 0;
     res->bytes_moved = h.bytes_moved;

@@ -36,6 +36,7 @@ constexpr int kLocalMax = 131072;     // segments <= this are partitioned by one
 constexpr int kLocalBig = 32768;      // local segments above this are scheduled first (LPT)
 constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
 constexpr int kFillDirect = 16;       // equality runs up to this are written by the emitting thread
+constexpr int kTinyGap = 16;          // gaps up to this are sorted by the emitting thread
 // segment sorter: one CTA sorts a whole segment on chip (shared-memory copy ->
 // interpolation buckets -> per-thread / per-warp bucket sorts).  Three size
 // classes, each with its own CTA shape so that every thread holds 12..16 keys:
@@ -57,7 +58,7 @@ __host__ __device__ constexpr int sort_lambda(int c) { return c == 0 ? KS_LAM0 :
 __host__ __device__ __forceinline__ int sort_class(long long len) { return len <= 2048 ? 0 : (len <= 6144 ? 1 : 2); }
 constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
 #ifndef KS_LOCAL_THREADS
-#define KS_LOCAL_THREADS 512
+#define KS_LOCAL_THREADS 1024
 #endif
 constexpr int kLocalThreads = KS_LOCAL_THREADS;   // CTA of the local partitioner
 constexpr int kUnitWarps = 8;         // warps per CTA of the unit sorter
@@ -77,11 +78,10 @@ struct DevStatus {
     unsigned int neg_zero;            // saw -0.0
     int nseg[2];                      // segment counts of the two level tables
     int nunits;                       // warp work items (unit sorts, fills) of the current pass
-    int nlocal[2];                    // local-partition segments (current round, next round)
-    int nlocal_big[2];                // ... of which > kLocalBig keys (stored from the top of the list)
-    int local_next;                   // dynamic work counter of the local round
-    int nsort[kSortClasses];          // segment-sorter lists, one per size class
-    int sort_next[kSortClasses];      // dynamic work counters of the segment sorter
+    // on-chip work queues of the leaf kernel (local partitions, segment sorts)
+    int lq_claim, lq_head;            // local queue: slots claimed by producers / taken by consumers
+    int sq_claim, sq_head;            // sort queue
+    int pending;                      // queued or running leaf items (the leaf kernel ends at zero)
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
@@ -120,12 +120,10 @@ struct Seg {
 enum ItemKind : int { kItemUnit = 0, kItemFill = 1 };
 struct Item {
     long long start;
-    long long tag;     // partition id (its segment start): only units of one partition are packed together
-    int len;
-    int kind;          // ItemKind
-    int src;           // 0: keys hold the data, 1: tmp holds the data
-    int pad;
     double value;      // fill value (the pivot of an equality run)
+    int len;
+    short kind;        // ItemKind
+    short src;         // 0: keys hold the data, 1: tmp holds the data
 };
 
 __device__ __forceinline__ void add_bytes(DevStatus *st, int phase, unsigned long long b)
