@@ -122,7 +122,17 @@ struct LeafQ {
     unsigned long long *sq_ready;
     int scap;
     int epoch;        // leaf launch these items belong to
+    Seg *small[2];    // segments of size classes 0 / 1: sorted by their own CTA shapes after the leaf launch
+    int small_cap[2];
 };
+
+// small segments (<= sort_cap(1) keys) go to the size-class lists
+__device__ __forceinline__ void small_push(const LeafQ &Q, const Seg &g, DevStatus *st)
+{
+    const int c = g.len <= sort_cap(0) ? 0 : 1;
+    const int i = atomicAdd(&st->nsmall[c], 1);
+    if (i < Q.small_cap[c]) (c ? Q.small[1] : Q.small[0])[i] = g; else st->overflow = 5;
+}
 
 __device__ __forceinline__ unsigned long long q_tag(int epoch, int idx)
 {
@@ -169,6 +179,10 @@ __device__ __forceinline__ Seg with_kind(Seg g, int kind)
 // single-item push to the sort queue (pending is raised before the slot can be claimed)
 __device__ __forceinline__ void q_push1(bool local, const LeafQ &Q, const Seg &g, DevStatus *st)
 {
+    if (!local && g.len <= sort_cap(1)) {
+        small_push(Q, g, st);
+        return;
+    }
     atomicAdd(&st->pending, 1);
     q_publish(Q.sq, Q.sq_ready, Q.scap, atomicAdd(&st->sq_claim, 1), with_kind(g, local ? kItemLocal : kItemSort),
               Q.epoch);
@@ -962,6 +976,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
             t_gap = 1;
         }
         else if (gl <= kUnitMax) u_gap = 1;
+        else if (gl <= sort_cap(1)) small_push(A.Q, make_seg(ag, gl, dst_id), st);
         else if (gl <= kSortMax) s_gap = 1;
         else if (gl <= kLocalMax) l_gap = 1;
         else g_gap = 1;
@@ -1488,6 +1503,38 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     }
 }
 
+// Small segments (size classes 0 and 1): persistent CTAs of the class's own
+// shape pull them from a counter after the leaf launch.  Hand-backs go to the
+// next leaf launch's queue.
+template <int C>
+__global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? 2 : 5)
+    k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp)
+{
+    KS_PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SortSmem<C> &S = *reinterpret_cast<SortSmem<C> *>(smem_raw);
+    __shared__ int s_item;
+    if (abort_requested(st)) return;
+    const int n = *count;
+    unsigned long long keys_sorted = 0, segs_sorted = 0;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
+        __syncthreads();
+        const int d = s_item;
+        if (d >= n) break;
+        const Seg g = list[d];
+        segsort_one<C>(S, g, Q, st, keys, tmp);
+        keys_sorted += (unsigned long long)g.len;
+        segs_sorted += 1;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && segs_sorted) {
+        add_bytes(st, kPhLeaf, 16ull * keys_sorted);
+        atomicAdd(&st->keys_leaf, keys_sorted);
+        atomicAdd(&st->leaves, segs_sorted);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // leaf kernel: one persistent CTA per SM drains the local queue (biggest work
 // first: each local partition feeds the sort queue) and then the sort queue,
@@ -1701,6 +1748,8 @@ FastLayout fast_layout(long long n, long long nseg0)
     // leaf queues: queued items are disjoint ranges of > kUnitMax keys, plus CTAs in flight
     L.lq_cap = (int)(n / (kUnitMax + 1) + nseg0 + 4096);
     L.sq_cap = L.lq_cap;
+    L.small_cap[0] = (int)(n / (kUnitMax + 1) + nseg0 + 2);      // disjoint ranges per leaf launch
+    L.small_cap[1] = (int)(n / (sort_cap(0) + 1) + nseg0 + 2);
     const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
@@ -1717,6 +1766,8 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.o_sq_ready = off; off = align_up(off + sizeof(unsigned long long) * L.sq_cap);   //  one clear per call)
     L.o_lq = off; off = align_up(off + sizeof(Seg) * L.lq_cap);
     L.o_sq = off; off = align_up(off + sizeof(Seg) * L.sq_cap);
+    L.o_small[0] = off; off = align_up(off + sizeof(Seg) * L.small_cap[0]);
+    L.o_small[1] = off; off = align_up(off + sizeof(Seg) * L.small_cap[1]);
     L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
     L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
     L.o_lut = off; off = align_up(off + sizeof(unsigned) * L.lut_cap);
@@ -1732,7 +1783,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 // Per-device launch shapes and kernel attributes, set up once per process
 // (cudaFuncSetAttribute / occupancy queries cost host time on every call).
 struct EngineCfg {
-    int sms, g_count, g_scatter, g_units, g_leaf;
+    int sms, g_count, g_scatter, g_units, g_leaf, g_small[2];
 };
 
 static const EngineCfg *engine_cfg()
@@ -1754,6 +1805,8 @@ static const EngineCfg *engine_cfg()
     smem(k_count<true>, sizeof(CountSmem));
     smem(k_count<false>, sizeof(CountSmem));
     smem(k_leaf, kLeafSmem);
+    smem(k_segsort<0>, sizeof(SortSmem<0>));
+    smem(k_segsort<1>, sizeof(SortSmem<1>));
     if (!ok) {
         fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
         return nullptr;
@@ -1768,6 +1821,8 @@ static const EngineCfg *engine_cfg()
     c.g_scatter = grid(k_scatter, kPassThreads, sizeof(ScatterSmem));
     c.g_units = grid(k_finish_units, kUnitWarps * 32, 0);
     c.g_leaf = grid(k_leaf, kLeafThreads, kLeafSmem);
+    c.g_small[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
+    c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -1791,7 +1846,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     double *tmp = reinterpret_cast<double *>(w + L.o_tmp);
     LeafQ Q{reinterpret_cast<Seg *>(w + L.o_lq), reinterpret_cast<unsigned long long *>(w + L.o_lq_ready), L.lq_cap,
             reinterpret_cast<Seg *>(w + L.o_sq), reinterpret_cast<unsigned long long *>(w + L.o_sq_ready), L.sq_cap,
-            1};
+            1, {reinterpret_cast<Seg *>(w + L.o_small[0]), reinterpret_cast<Seg *>(w + L.o_small[1])},
+            {L.small_cap[0], L.small_cap[1]}};
 
     const EngineCfg *cfg = engine_cfg();
     if (cfg == nullptr) return KS_CUDA_ERROR;
@@ -1881,22 +1937,36 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         ++level;
         gcur ^= 1;
     };
-    // leaf launch: queues -> sorted ranges, then the warp units and fills
+    // leaf launch: queues -> sorted ranges; then the small segments by their own
+    // CTA shapes (hand-backs go to the next leaf epoch), the warp units and fills
     auto leaf = [&]() {
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1};
         K.run(kPhLeaf, [&] { launch(k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head);
+        LeafQ Qn = Q;
+        ++Qn.epoch;
+        K.run(kPhLeaf, [&] {
+            launch(k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, Q.small[1],
+                   &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp);
+        });
+        K.run(kPhLeaf, [&] {
+            launch(k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
+                   &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp);
+        });
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nsmall[0], &st->nsmall[1], &st->small_next[0],
+               &st->small_next[1]);
         K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
         launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nunits, (int *)nullptr, (int *)nullptr, (int *)nullptr);
-        ++Q.epoch;
+        Q = Qn;
         ++leaves_run;
     };
     if (n > kLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
     leaf();
     int rc = sync_status();
     if (rc != KS_OK) return rc;
-    while (!aborted() && h.nseg[gcur] > 0) {   // remaining work (rare): more global levels
-        global_pass();
+    // remaining work (rare): more global levels, or hand-backs queued for another leaf launch
+    while (!aborted() && (h.nseg[gcur] > 0 || h.sq_claim > 0 || h.lq_claim > 0)) {
+        if (h.nseg[gcur] > 0) global_pass();
         leaf();
         rc = sync_status();
         if (rc != KS_OK) return rc;

@@ -82,6 +82,8 @@ struct DevStatus {
     int lq_claim, lq_head;            // local queue: slots claimed by producers / taken by consumers
     int sq_claim, sq_head;            // sort queue
     int pending;                      // queued or running leaf items (the leaf kernel ends at zero)
+    int nsmall[2];                    // small-segment lists (size classes 0, 1), sorted after the leaf launch
+    int small_next[2];                // their work counters
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
