@@ -1164,6 +1164,7 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
         const int c = classify(v, L.piv, L.lut, lo, scale, T);
         if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v;
     }
+    __threadfence();   // children are published below and may be taken by other SMs at once
     __syncthreads();
     KS_TR(2);
     // class starts = cursor - (keys written); emit per pivot pair
@@ -1293,8 +1294,9 @@ struct SortSmem {
     double red[2][32];
     double bounds[2];      // lo, scale
     unsigned sh[33];
-    long long start;       // descriptor of the segment being processed (prefetched by thread 0)
-    int len, src, item, nbig;
+    int nbig;
+    int nhb;               // hand-back buckets (published once the segment is written)
+    int hb[kCap / (kUnitMax + 1) + 1];
 };
 
 __device__ __forceinline__ int sort_bucket(double v, double lo, double scale, int B)
@@ -1403,7 +1405,10 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
 #pragma unroll 1
     for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
-    if (tid == 0) S.nbig = 0;
+    if (tid == 0) {
+        S.nbig = 0;
+        S.nhb = 0;
+    }
     __syncthreads();
     if (wid == 0) {   // block min / max and the bucket scale, broadcast through shared memory
         mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
@@ -1475,7 +1480,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 const int s0 = b ? (int)S.cur[b - 1] : 0;
                 const int sz = (int)S.cur[b] - s0;
                 if (!warp_sort_bucket(S.b + s0, sz) && lane == 0)   // skewed: back to the first-key partitioner
-                    q_push1(true, Q, make_seg(start + s0, sz, 0), st);
+                    S.hb[atomicAdd(&S.nhb, 1)] = b;
             }
             __syncthreads();
         }
@@ -1499,6 +1504,14 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 pos = r;
             }
             out[pos] = x;
+        }
+        // hand-backs are published only once their keys are in place
+        __syncthreads();
+        if (tid < S.nhb) {
+            const int b = S.hb[tid];
+            const int s0 = b ? (int)S.cur[b - 1] : 0;
+            __threadfence();
+            q_push1(true, Q, make_seg(start + s0, (int)S.cur[b] - s0, 0), st);
         }
     }
 }

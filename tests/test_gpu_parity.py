@@ -403,3 +403,48 @@ def test_sizes_around_thresholds():
         t = dev(a)
         K.k_sort(t)
         assert same_bits(host(t), np.sort(a)), n
+
+
+def _skewed(kind, n, rng):
+    if kind == "exponential":
+        return rng.exponential(1.0, n)
+    if kind == "lognormal":
+        return rng.lognormal(0.0, 4.0, n)
+    if kind == "normal":
+        return rng.normal(0.0, 1.0, n)
+    if kind == "clusters":   # a few very narrow clusters far apart
+        centers = rng.uniform(-1e6, 1e6, 7)
+        return centers[rng.integers(0, 7, n)] + rng.normal(0.0, 1e-9, n)
+    if kind == "powers_of_two":   # exponentially spaced values: worst case for interpolation buckets
+        return np.ldexp(1.0, rng.integers(-1000, 1000, n)) * rng.choice([-1.0, 1.0], n)
+    if kind == "small_integers":
+        return rng.integers(0, 1000, n).astype(np.float64)
+    if kind == "bit_patterns":   # random finite doubles over the whole exponent range
+        u = rng.integers(0, 2**63, n, dtype=np.int64).view(np.float64)
+        u[~np.isfinite(u)] = 1.0
+        u[u == 0.0] = 1.0   # keep signed zeros out of the fast-engine bitwise contract
+        return u * rng.choice([-1.0, 1.0], n)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["exponential", "lognormal", "normal", "clusters", "powers_of_two",
+                                  "small_integers", "bit_patterns"])
+@pytest.mark.parametrize("n", [300_001, 3_000_000])
+def test_skewed_distributions(kind, n):
+    """Value distributions that defeat the segment sorter's interpolation buckets
+    (oversized buckets, hand-backs to the first-key partitioner) must still sort exactly."""
+    rng = np.random.default_rng(hash((kind, n)) % 2**32)
+    a = _skewed(kind, n, rng)
+    t = dev(a)
+    K.k_sort(t)
+    assert same_bits(host(t), np.sort(a)), kind
+
+
+def test_sizes_around_engine_limits():
+    """Sizes at every routing threshold (tiny gap, unit, sort classes, on-chip sort, local partition)."""
+    rng = np.random.default_rng(3)
+    for n in (16, 17, 512, 513, 2048, 2049, 6144, 6145, 12288, 12289, 131072, 131073, 262147):
+        a = rng.random(n)
+        t = dev(a)
+        K.k_sort(t)
+        assert same_bits(host(t), np.sort(a)), n
