@@ -196,11 +196,11 @@ struct InitLists {
     int seg_cap, unit_cap;
 };
 
-// > kLocalMax keys -> global pass list, kSortMax < len <= kLocalMax -> local
-// queue, kUnitMax < len <= kSortMax -> sort queue, 2..kUnitMax -> unit.
+// > kInitLocalMax keys -> global pass list, kSortMax < len <= kInitLocalMax ->
+// local queue, kUnitMax < len <= kSortMax -> sort queue, 2..kUnitMax -> unit.
 __device__ __forceinline__ void route_initial(long long a, long long len, const InitLists &Lst, DevStatus *st)
 {
-    if (len > kLocalMax) {
+    if (len > kInitLocalMax) {   // (a lone large array is partitioned by all SMs, not by one CTA)
         int i = atomicAdd(&st->nseg[0], 1);
         if (i < Lst.seg_cap) Lst.gsegs[i] = make_seg(a, len, 0); else st->overflow = 1;
     } else if (len > kUnitMax) {
@@ -253,7 +253,7 @@ __device__ __forceinline__ void gate_flush(long long bad, unsigned pz, unsigned 
 }
 
 // Finiteness gate (sort_core.py:50-59) for keys not covered by the level-0
-// count pass: segments of <= kLocalMax keys (they never see a global pass).
+// count pass: segments of <= kInitLocalMax keys (they never see a global pass).
 __global__ void k_gate_segments(const double *keys, const long long *off, long long nseg0, long long n_single,
                                 DevStatus *st)
 {
@@ -270,7 +270,7 @@ __global__ void k_gate_segments(const double *keys, const long long *off, long l
     } else {
         for (long long s = blockIdx.x; s < nseg0; s += gridDim.x) {
             long long a = off[s], b = off[s + 1];
-            if (b - a > kLocalMax) continue;  // covered by the level-0 count pass
+            if (b - a > kInitLocalMax) continue;  // covered by the level-0 count pass
             for (long long i = a + threadIdx.x; i < b; i += blockDim.x) {
                 gate_one(keys[i], i, bad, pz, nz);
                 ++checked;
@@ -1757,7 +1757,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 {
     FastLayout L{};
     L.n = n;
-    L.seg_cap = (int)(n / (kLocalMax + 1) + 2);                  // global-pass segments
+    L.seg_cap = (int)(n / (kInitLocalMax + 1) + 2);              // global-pass segments (level 0: > kInitLocalMax)
     // leaf queues: queued items are disjoint ranges of > kUnitMax keys, plus CTAs in flight
     L.lq_cap = (int)(n / (kUnitMax + 1) + nseg0 + 4096);
     L.sq_cap = L.lq_cap;
@@ -1888,7 +1888,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
     if (d_off == nullptr) {
         K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
-        if (n <= kLocalMax)
+        if (n <= kInitLocalMax)
             K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
     } else {
         K.run(kPhGate, [&] { launch(k_init_segmented, dim3(sms), dim3(256), 0, stream, d_off, nseg0, Lst, st); });
@@ -1973,7 +1973,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         Q = Qn;
         ++leaves_run;
     };
-    if (n > kLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
+    if (n > kInitLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
     leaf();
     int rc = sync_status();
     if (rc != KS_OK) return rc;

@@ -33,6 +33,7 @@ constexpr int kCountThreads = 512;
 constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
 constexpr int kPassThreads = 512;     // threads of scatter CTAs (8 keys each per tile)
 constexpr int kLocalMax = 131072;     // segments <= this are partitioned by one CTA (L2-resident)
+constexpr int kInitLocalMax = 24576;  // ... for input arrays / batch segments (few items: use all SMs)
 constexpr int kLocalBig = 32768;      // local segments above this are scheduled first (LPT)
 constexpr int kUnitMax = 512;         // largest run one warp sorts in registers (16 per lane)
 constexpr int kFillDirect = 16;       // equality runs up to this are written by the emitting thread
