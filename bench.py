@@ -52,6 +52,19 @@ def parse():
     return p.parse_args()
 
 
+def ncu_traffic(phase, n, kind):
+    """DRAM bytes per launch of `phase` from the committed ncu --set full capture
+    (profiles/ncu_traffic.json), when it was taken on this workload; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            d = json.load(fh)
+        if f"{n:,}" in d["workload"] and kind in d["workload"] and phase in d["phases"]:
+            return d["phases"][phase]["dram_bytes_per_launch"]
+    except Exception:
+        pass
+    return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -316,7 +329,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "correct": ok,
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": dom_gbs / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "frac": dom_gbs / hbm, "traffic": ncu_traffic(dom, n, args.kind), "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": phase[dom]["bytes"] / max(1, phase[dom]["launches"])},
         "multi_pass": {"bytes_per_sort": stats.bytes_moved, "bytes_per_key": stats.bytes_moved / n,
                        "achieved_gbs": multi_pass_gbs, "frac_of_measured": multi_pass_gbs / hbm,

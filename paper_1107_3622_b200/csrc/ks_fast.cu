@@ -1036,8 +1036,8 @@ __device__ __forceinline__ void account_partition(DevStatus *st, long long len, 
 {
     // algorithmic bytes: count reads 8B/key; scatter reads 8B/key and writes 8B
     // per key it places; units read+write 16B/key; fills write 8B/key
-    add_bytes(st, local ? kPhOther : kPhCount, 8ull * len);
-    add_bytes(st, local ? kPhOther : kPhScatter, 8ull * len + 8ull * (len - o.fill_keys));
+    add_bytes(st, local ? kPhLeaf : kPhCount, 8ull * len);
+    add_bytes(st, local ? kPhLeaf : kPhScatter, 8ull * len + 8ull * (len - o.fill_keys));
     add_bytes(st, kPhLeaf, 16ull * o.unit_keys + 8ull * o.fill_keys);
     atomicAdd(&st->keys_partitioned, (unsigned long long)len);
     atomicAdd(&st->keys_leaf, (unsigned long long)o.unit_keys);
