@@ -30,7 +30,7 @@ namespace ks {
 
 #ifdef KS_TRACE
 // optional phase-cycle instrumentation (build with KS_TRACE=1), read via ks_trace_read
-__device__ unsigned long long g_trace[16];
+__device__ unsigned long long g_trace[32];
 #define KS_TR_DECL long long tr_t0 = clock64()
 #define KS_TR(slot)                                                                  \
     do {                                                                             \
@@ -60,6 +60,9 @@ __device__ unsigned long long g_trace[16];
 #endif
 #ifndef KS_PDL
 #define KS_PDL 1          // programmatic dependent launch between the engine's kernels
+#endif
+#ifndef KS_RANK_LEAF
+#define KS_RANK_LEAF 0    // 1: in-bucket ranks per key instead of per-bucket networks
 #endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
@@ -1295,6 +1298,7 @@ struct SortSmem {
     double bounds[2];      // lo, scale
     unsigned sh[33];
     int nbig;
+    int nmid;              // buckets of 5..kThreadSortMax keys (listed in the free `a` buffer)
     int nhb;               // hand-back buckets (published once the segment is written)
     int hb[kCap / (kUnitMax + 1) + 1];
 };
@@ -1363,6 +1367,19 @@ template <int C>
 __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevStatus *st, double *keys,
                             const double *tmp)
 {
+#ifdef KS_TRACE
+    long long tr_t0 = clock64();
+#define KS_TRS(slot)                                                                    \
+    do {                                                                                \
+        if (threadIdx.x == 0) {                                                         \
+            long long t1_ = clock64();                                                  \
+            atomicAdd(&g_trace[16 + 5 * C + (slot)], (unsigned long long)(t1_ - tr_t0)); \
+            tr_t0 = t1_;                                                                \
+        }                                                                               \
+    } while (0)
+#else
+#define KS_TRS(slot)
+#endif
     using Smem = SortSmem<C>;
     constexpr int kT = Smem::kT;
     constexpr int kWarps = kT / 32;
@@ -1374,15 +1391,16 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     double *out = keys + start;
     // 1. load (coalesced, 4 loads in flight per thread, L2 only) + min / max
     double mn = CUDART_INF, mx = -CUDART_INF;
-    for (int i0 = 0; i0 < m; i0 += 4 * kT) {
-        double x[4];
+    constexpr int kLU = kT >= 1024 ? 4 : 8;   // loads in flight per thread (one round trip for most segments)
+    for (int i0 = 0; i0 < m; i0 += kLU * kT) {
+        double x[kLU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kLU; ++u) {
             const int i = i0 + u * kT + tid;
             x[u] = i < m ? __ldcg(in + i) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kLU; ++u) {
             const int i = i0 + u * kT + tid;
             if (i < m) {
                 S.a[i] = x[u];
@@ -1429,6 +1447,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     __syncthreads();
     const double lo = S.bounds[0];
     const double scale = S.bounds[1];
+    KS_TRS(0);   // load + min/max
     if (scale < 0.0) {   // constant segment: already sorted
         if (g.src) {
 #pragma unroll 1
@@ -1440,6 +1459,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 #pragma unroll 1
         for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[sort_bucket(S.a[i], lo, scale, B)], 1u);
         __syncthreads();
+        KS_TRS(1);   // histogram
         {
             const int b0 = tid * Smem::kPB;
             unsigned c[Smem::kPB];
@@ -1470,6 +1490,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             S.b[atomicAdd(&S.cur[sort_bucket(x, lo, scale, B)], 1u)] = x;
         }
         __syncthreads();
+        KS_TRS(2);   // scan + scatter
         // 3. cur[b] is now the end of bucket b.  Buckets of more than
         //    kThreadSortMax keys (listed by the scan; none for smooth
         //    inputs) are sorted in place by one warp each.
@@ -1484,6 +1505,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             }
             __syncthreads();
         }
+#if KS_RANK_LEAF
         // 4. every key of a small bucket takes its rank inside the bucket
         //    (ties by position: equal keys are bitwise equal here) and is
         //    written straight to its final place
@@ -1505,8 +1527,58 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             }
             out[pos] = x;
         }
+#else
+        // 4a. one thread per bucket: <= 4 keys -> sorting network in registers,
+        //     stored straight to the final place; 5..kThreadSortMax keys ->
+        //     listed (the `a` buffer is free now) for 4b
+        int *mid = reinterpret_cast<int *>(S.a);
+        if (tid == 0) S.nmid = 0;
+        __syncthreads();
+#pragma unroll 1
+        for (int b = tid; b < B; b += kT) {
+            const int s0 = b ? (int)S.cur[b - 1] : 0;
+            const int sz = (int)S.cur[b] - s0;
+            if (sz == 0 || sz > kThreadSortMax) continue;
+            if (sz <= 4) {
+                const double *x = S.b + s0;
+                double x0 = x[0], x1 = sz > 1 ? x[1] : CUDART_INF, x2 = sz > 2 ? x[2] : CUDART_INF,
+                       x3 = sz > 3 ? x[3] : CUDART_INF;
+                cas(x0, x1, true);
+                cas(x2, x3, true);
+                cas(x0, x2, true);
+                cas(x1, x3, true);
+                cas(x1, x2, true);
+                double *o = out + s0;
+                o[0] = x0;
+                if (sz > 1) o[1] = x1;
+                if (sz > 2) o[2] = x2;
+                if (sz > 3) o[3] = x3;
+            } else {
+                mid[atomicAdd(&S.nmid, 1)] = b;
+            }
+        }
+        __syncthreads();
+        // 4b. 5..kThreadSortMax keys: one thread each, insertion sort in shared memory
+        const int nmid = S.nmid;
+#pragma unroll 1
+        for (int q = tid; q < nmid; q += kT) {
+            const int b = mid[q];
+            const int s0 = b ? (int)S.cur[b - 1] : 0;
+            const int sz = (int)S.cur[b] - s0;
+            smem_insertion_sort(S.b + s0, sz);
+            for (int i = 0; i < sz; ++i) out[s0 + i] = S.b[s0 + i];
+        }
+        // 4c. large buckets (sorted by warps above, or handed back): coalesced copy
+        for (int q = wid; q < nbig; q += kWarps) {
+            const int b = S.big[q];
+            const int s0 = b ? (int)S.cur[b - 1] : 0;
+            const int sz = (int)S.cur[b] - s0;
+            for (int i = lane; i < sz; i += 32) out[s0 + i] = S.b[s0 + i];
+        }
+#endif
         // hand-backs are published only once their keys are in place
         __syncthreads();
+        KS_TRS(3);   // big buckets + in-bucket order + write
         if (tid < S.nhb) {
             const int b = S.hb[tid];
             const int s0 = b ? (int)S.cur[b - 1] : 0;
@@ -1514,6 +1586,10 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             q_push1(true, Q, make_seg(start + s0, (int)S.cur[b] - s0, 0), st);
         }
     }
+#ifdef KS_TRACE
+    if (threadIdx.x == 0) atomicAdd(&g_trace[16 + 5 * C + 4], 1ull);
+#endif
+#undef KS_TRS
 }
 
 // Small segments (size classes 0 and 1): persistent CTAs of the class's own
@@ -1530,12 +1606,32 @@ __global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? 2 : 
     if (abort_requested(st)) return;
     const int n = *count;
     unsigned long long keys_sorted = 0, segs_sorted = 0;
+    // thread 0 claims one item ahead and pulls its input and output ranges into
+    // L2 while the current one is sorted (a cold segment otherwise costs two
+    // DRAM round trips to load and a fill stall per partially written sector)
+    auto prefetch = [&](int d) {
+#if KS_PREFETCH
+        if (d < n) {
+            const Seg g = list[d];
+            l2_prefetch((g.src ? tmp : keys) + g.start, 8ull * g.len);
+            if (g.src) l2_prefetch(keys + g.start, 8ull * g.len);
+        }
+#endif
+    };
+    if (threadIdx.x == 0) {
+        s_item = atomicAdd(next, 1);
+        prefetch(s_item);
+    }
     for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(next, 1);
         __syncthreads();
         const int d = s_item;
         if (d >= n) break;
         const Seg g = list[d];
+        __syncthreads();   // everyone has read s_item
+        if (threadIdx.x == 0) {
+            s_item = atomicAdd(next, 1);
+            prefetch(s_item);
+        }
         segsort_one<C>(S, g, Q, st, keys, tmp);
         keys_sorted += (unsigned long long)g.len;
         segs_sorted += 1;
@@ -2002,11 +2098,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 #ifdef KS_TRACE
 extern "C" int ks_trace_read(unsigned long long *out, int n, int reset)
 {
-    unsigned long long h[16];
+    unsigned long long h[32];
     cudaMemcpyFromSymbol(h, ks::g_trace, sizeof(h));
-    for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
+    for (int i = 0; i < n && i < 32; ++i) out[i] = h[i];
     if (reset) {
-        unsigned long long z[16] = {0};
+        unsigned long long z[32] = {0};
         cudaMemcpyToSymbol(ks::g_trace, z, sizeof(z));
     }
     return 0;

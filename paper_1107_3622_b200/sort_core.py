@@ -30,6 +30,7 @@ Engines (all on the GPU; there is no CPU fallback):
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass
 from typing import Callable, Optional, Union
 
@@ -90,8 +91,36 @@ def _stream_ptr() -> int:
     return torch.cuda.current_stream().cuda_stream
 
 
+_tls = threading.local()
+
+
 def _workspace(nbytes: int) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=_device())
+    """Per-thread, per-device scratch buffer, grown on demand and reused: the
+    library never allocates, and calls are synchronous, so one buffer per
+    calling thread is enough (distinct threads may sort concurrently)."""
+    nbytes = max(int(nbytes), 256)
+    dev = _device()
+    cache = getattr(_tls, "ws", None)
+    if cache is None:
+        cache = _tls.ws = {}
+    buf = cache.get(dev.index)
+    if buf is None or buf.numel() < nbytes:
+        cache[dev.index] = None   # release the old buffer before growing
+        buf = cache[dev.index] = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    return buf
+
+
+_ws_sizes: dict = {}
+
+
+def _workspace_bytes(L, n: int, nseg: int, flags: int) -> int:
+    key = (n, nseg, flags)
+    v = _ws_sizes.get(key)
+    if v is None:
+        v = _ws_sizes[key] = int(L.ks_workspace_bytes(n, nseg, flags))
+        if len(_ws_sizes) > 4096:
+            _ws_sizes.clear()
+    return v
 
 
 class _Staged:
@@ -159,13 +188,13 @@ def _sort_device(keys: torch.Tensor, flags: int = 0) -> _lib.KsStatus:
     L = _lib.load()
     n = keys.numel()
     st = _lib.KsStatus()
-    ws_bytes = L.ks_workspace_bytes(n, 1, flags)
+    ws_bytes = _workspace_bytes(L, n, 1, flags)
     ws = _workspace(ws_bytes)
     code = L.ks_sort_f64(keys.data_ptr(), n, ws.data_ptr(), ws_bytes, _stream_ptr(), flags,
                          ctypes.byref(st))
     if code == _lib.KS_NEED_EXACT:
         # both signed zeros present: rerun with the exact engine's workspace
-        ws_bytes = L.ks_workspace_bytes(n, 1, flags | _lib.KS_FLAG_EXACT)
+        ws_bytes = _workspace_bytes(L, n, 1, flags | _lib.KS_FLAG_EXACT)
         ws = _workspace(ws_bytes)
         code = L.ks_sort_f64(keys.data_ptr(), n, ws.data_ptr(), ws_bytes, _stream_ptr(), flags,
                              ctypes.byref(st))
