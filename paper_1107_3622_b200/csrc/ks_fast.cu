@@ -64,6 +64,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_RANK_LEAF
 #define KS_RANK_LEAF 0    // 1: in-bucket ranks per key instead of per-bucket networks
 #endif
+#ifndef KS_GRAPH
+#define KS_GRAPH 1        // replay the speculative schedule as a cached CUDA graph
+#endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
 #endif
@@ -1937,9 +1940,93 @@ static const EngineCfg *engine_cfg()
     return &cfgs[dev];
 }
 
-int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
-              cudaStream_t stream, bool profile, FastResult *res)
+// CUDA-graph cache of the speculative schedule.  Its launches depend only on
+// the buffers and sizes of the call (the device decides everything else), so a
+// repeated call with the same (keys, offsets, workspace, n) replays one graph
+// instead of ~20 launches.  Captured on an internal stream (the caller's may
+// be the legacy default stream, which cannot capture) and launched on the
+// caller's stream.  Small LRU, one per process.
+struct GraphKey {
+    const void *keys, *d_off, *ws;
+    long long n, nseg0;
+    size_t ws_bytes;
+    bool operator==(const GraphKey &o) const
+    {
+        return keys == o.keys && d_off == o.d_off && ws == o.ws && n == o.n && nseg0 == o.nseg0 &&
+               ws_bytes == o.ws_bytes;
+    }
+};
+struct GraphEntry {
+    GraphKey key;
+    int dev;
+    cudaGraphExec_t exec;
+    int level, gcur, leaves_run, epoch, launches;
+    unsigned long long last_use;
+};
+static std::mutex g_graph_mu;
+static std::vector<GraphEntry> g_graphs;
+static unsigned long long g_graph_clock = 0;
+constexpr size_t kGraphCacheMax = 8;
+
+// Copies out of the cache under the lock.  A graph is captured on the second
+// call with the same key (a one-off call runs the launches directly: capture
+// and instantiation would cost more than they save).
+static bool graph_lookup(const GraphKey &k, GraphEntry *out, bool *seen_before)
 {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (auto &e : g_graphs)
+        if (e.dev == dev && e.key == k) {
+            e.last_use = ++g_graph_clock;
+            *out = e;
+            return true;
+        }
+    static GraphKey seen[kGraphCacheMax];
+    static int seen_dev[kGraphCacheMax];
+    static size_t seen_next = 0;
+    *seen_before = false;
+    for (size_t i = 0; i < kGraphCacheMax; ++i)
+        if (seen[i] == k && seen_dev[i] == dev) *seen_before = true;
+    if (!*seen_before) {
+        seen[seen_next % kGraphCacheMax] = k;
+        seen_dev[seen_next % kGraphCacheMax] = dev;
+        ++seen_next;
+    }
+    return false;
+}
+
+static void graph_store(GraphEntry e)
+{
+    cudaGetDevice(&e.dev);
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    e.last_use = ++g_graph_clock;
+    if (g_graphs.size() >= kGraphCacheMax) {
+        size_t victim = 0;
+        for (size_t i = 1; i < g_graphs.size(); ++i)
+            if (g_graphs[i].last_use < g_graphs[victim].last_use) victim = i;
+        cudaGraphExecDestroy(g_graphs[victim].exec);
+        g_graphs.erase(g_graphs.begin() + victim);
+    }
+    g_graphs.push_back(e);
+}
+
+static cudaStream_t capture_stream()
+{
+    static std::mutex mu;
+    static cudaStream_t streams[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    if (streams[dev] == nullptr && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
+        return nullptr;
+    return streams[dev];
+}
+
+int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
+              cudaStream_t user_stream, bool profile, FastResult *res)
+{
+    cudaStream_t stream = user_stream;   // (the capture stream while a graph is being recorded)
     FastLayout L = fast_layout(n, nseg0);
     if (ws_bytes < L.total) return KS_WORKSPACE_SMALL;
     char *w = static_cast<char *>(ws);
@@ -1975,21 +2062,23 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     };
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
 
-    // queue ready words: cleared once per call (their tags carry the leaf epoch)
-    KS_CK(cudaMemsetAsync(Q.lq_ready, 0, L.o_lq - L.o_lq_ready, stream));
-    if (d_off != nullptr) {   // (the single-array init kernel clears the status itself)
-        KS_CK(cudaMemsetAsync(st, 0, sizeof(DevStatus), stream));
-        KS_CK(cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream));
-    }
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
-    if (d_off == nullptr) {
-        K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
-        if (n <= kInitLocalMax)
-            K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
-    } else {
-        K.run(kPhGate, [&] { launch(k_init_segmented, dim3(sms), dim3(256), 0, stream, d_off, nseg0, Lst, st); });
-        K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 4), dim3(256), 0, stream, keys, d_off, nseg0, 0, st); });
-    }
+    auto init_launch = [&]() {
+        // queue ready words: cleared once per call (their tags carry the leaf epoch)
+        cudaMemsetAsync(Q.lq_ready, 0, L.o_lq - L.o_lq_ready, stream);
+        if (d_off != nullptr) {   // (the single-array init kernel clears the status itself)
+            cudaMemsetAsync(st, 0, sizeof(DevStatus), stream);
+            cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream);
+        }
+        if (d_off == nullptr) {
+            K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
+            if (n <= kInitLocalMax)
+                K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
+        } else {
+            K.run(kPhGate, [&] { launch(k_init_segmented, dim3(sms), dim3(256), 0, stream, d_off, nseg0, Lst, st); });
+            K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 4), dim3(256), 0, stream, keys, d_off, nseg0, 0, st); });
+        }
+    };
 
     // The schedule is launched speculatively without host round-trips: global
     // passes read their segment counts on the device (and exit at once when
@@ -2069,8 +2158,54 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         Q = Qn;
         ++leaves_run;
     };
-    if (n > kInitLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
-    leaf();
+    auto spec = [&]() {
+        init_launch();
+        if (n > kInitLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
+        leaf();
+    };
+    int launches_graph = 0;
+    bool replayed = false;
+    if (KS_GRAPH && !profile) {
+        // the speculative schedule depends only on (buffers, sizes): replay it as one CUDA graph
+        const GraphKey key{keys, d_off, ws, n, nseg0, ws_bytes};
+        GraphEntry e{};
+        bool seen = false;
+        bool have = graph_lookup(key, &e, &seen);
+        if (!have && seen) {
+            cudaStream_t cs = capture_stream();
+            if (cs == nullptr) return KS_CUDA_ERROR;
+            e.key = key;
+            stream = cs;
+            KS_CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            spec();
+            cudaGraph_t g = nullptr;
+            const cudaError_t ce = cudaStreamEndCapture(cs, &g);
+            stream = user_stream;
+            if (ce != cudaSuccess) {
+                fprintf(stderr, "ksort: graph capture failed: %s\n", cudaGetErrorString(ce));
+                return KS_CUDA_ERROR;
+            }
+            KS_CK(cudaGraphInstantiate(&e.exec, g, 0));
+            cudaGraphDestroy(g);
+            e.level = level;
+            e.gcur = gcur;
+            e.leaves_run = leaves_run;
+            e.epoch = Q.epoch;
+            e.launches = K.total();
+            graph_store(e);
+            have = true;
+        }
+        if (have) {
+            KS_CK(cudaGraphLaunch(e.exec, stream));
+            level = e.level;
+            gcur = e.gcur;
+            leaves_run = e.leaves_run;
+            Q.epoch = e.epoch;
+            launches_graph = e.launches - K.total();   // (the capture's launches were counted by K)
+            replayed = true;
+        }
+    }
+    if (!replayed) spec();
     int rc = sync_status();
     if (rc != KS_OK) return rc;
     // remaining work (rare): more global levels, or hand-backs queued for another leaf launch
@@ -2087,7 +2222,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     res->keys_partitioned = h.keys_partitioned;
     res->keys_leaf = h.keys_leaf;
     res->leaves = (long long)h.leaves;
-    res->launches = K.total();
+    res->launches = K.total() + launches_graph;
     K.collect(res->phase_ms, res->phase_launches);
     for (int p = 0; p < 8; ++p) res->phase_bytes[p] = h.phase_bytes[p];
     return KS_OK;
