@@ -1538,11 +1538,18 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         if (tid == 0) S.nmid = 0;
         __syncthreads();
 #pragma unroll 1
-        for (int b = tid; b < B; b += kT) {
-            const int s0 = b ? (int)S.cur[b - 1] : 0;
-            const int sz = (int)S.cur[b] - s0;
-            if (sz == 0 || sz > kThreadSortMax) continue;
-            if (sz <= 4) {
+        for (int b0 = tid; b0 < B; b0 += 2 * kT) {   // two buckets in flight per thread
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int b = b0 + h * kT;
+                if (b >= B) break;
+                const int s0 = b ? (int)S.cur[b - 1] : 0;
+                const int sz = (int)S.cur[b] - s0;
+                if (sz == 0 || sz > kThreadSortMax) continue;
+                if (sz > 4) {
+                    mid[atomicAdd(&S.nmid, 1)] = b;
+                    continue;
+                }
                 const double *x = S.b + s0;
                 double x0 = x[0], x1 = sz > 1 ? x[1] : CUDART_INF, x2 = sz > 2 ? x[2] : CUDART_INF,
                        x3 = sz > 3 ? x[3] : CUDART_INF;
@@ -1556,8 +1563,6 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 if (sz > 1) o[1] = x1;
                 if (sz > 2) o[2] = x2;
                 if (sz > 3) o[3] = x3;
-            } else {
-                mid[atomicAdd(&S.nmid, 1)] = b;
             }
         }
         __syncthreads();
