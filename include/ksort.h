@@ -103,6 +103,12 @@ int ks_heap_sort_f64_exact(double *d_keys, int64_t n, void *d_ws, size_t ws_byte
 int ks_is_sorted_f64(const double *d_keys, int64_t n, void *d_ws, void *stream,
                      int32_t *h_result);
 
+/* Replaces the finiteness checks on ingestion, workload._require_finite
+ * (workload.py:129-134) and sort_core._check_finite (sort_core.py:50-59):
+ * *h_index = first position holding NaN/+-inf, or -1.  Needs 8 bytes of
+ * workspace. */
+int ks_first_nonfinite_f64(const double *d_keys, int64_t n, void *d_ws, void *stream, int64_t *h_index);
+
 /* Device twin of workload._bulk_uniform01 (workload.py:68-78):
  * d_out[t] = (mix64(seed + (t+1)*0x9E3779B97F4A7C15) >> 11) * 2^-53.
  * kind 0 = uniform01, kind 1 = dup256 ((u >> 56) / 256, BASELINE configs[4]). */

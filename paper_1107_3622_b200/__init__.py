@@ -20,9 +20,10 @@ from .sort_core import (  # noqa: F401
     ksort_partition,
     last_stats,
 )
-from .workload import generate_device  # noqa: F401
+from .workload import generate_device, read_binary, read_text, write_binary, write_text  # noqa: F401
 
 __all__ = [
     "SORTERS", "KeyArray", "NonFiniteKeyError", "OpCounts", "PartitionOutcome", "SortStats",
     "heap_sort", "is_sorted", "k_sort", "k_sort_segments", "ksort_partition", "generate_device", "last_stats",
+    "read_binary", "write_binary", "read_text", "write_text",
 ]

@@ -26,7 +26,7 @@ PHASES = ("gate", "pivots", "count", "scan", "scatter", "plan", "leaf", "local")
 
 EXPORTED = (
     "ks_workspace_bytes", "ks_sort_f64", "ks_sort_f64_segmented", "ks_partition_f64",
-    "ks_heap_sort_f64_exact", "ks_is_sorted_f64", "ks_generate_f64", "ks_version",
+    "ks_heap_sort_f64_exact", "ks_is_sorted_f64", "ks_first_nonfinite_f64", "ks_generate_f64", "ks_version",
 )
 
 
@@ -86,6 +86,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.ks_heap_sort_f64_exact.restype = ctypes.c_int
     L.ks_is_sorted_f64.argtypes = [vp, i64, vp, vp, ctypes.POINTER(ctypes.c_int32)]
     L.ks_is_sorted_f64.restype = ctypes.c_int
+    L.ks_first_nonfinite_f64.argtypes = [vp, i64, vp, vp, ctypes.POINTER(ctypes.c_int64)]
+    L.ks_first_nonfinite_f64.restype = ctypes.c_int
     L.ks_generate_f64.argtypes = [vp, i64, ctypes.c_uint64, ctypes.c_int32, vp]
     L.ks_generate_f64.restype = ctypes.c_int
     L.ks_version.argtypes = []

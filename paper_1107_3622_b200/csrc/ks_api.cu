@@ -240,6 +240,15 @@ int ks_is_sorted_f64(const double *d_keys, int64_t n, void *d_ws, void *stream, 
     return rc;
 }
 
+int ks_first_nonfinite_f64(const double *d_keys, int64_t n, void *d_ws, void *stream, int64_t *h_index)
+{
+    if (n < 0 || !h_index || !d_ws || (n > 0 && !d_keys)) return KS_BAD_ARG;
+    long long bad = -1;
+    const int rc = gate_range(d_keys, n, d_ws, static_cast<cudaStream_t>(stream), &bad);
+    *h_index = bad;
+    return rc;
+}
+
 int ks_generate_f64(double *d_out, int64_t n, uint64_t seed, int32_t kind, void *stream)
 {
     if (n < 0 || (n > 0 && !d_out) || (kind != 0 && kind != 1)) return KS_BAD_ARG;
