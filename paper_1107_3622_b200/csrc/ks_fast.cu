@@ -427,6 +427,19 @@ __host__ __device__ __forceinline__ int lut_for(int P, int tmax)
 // ---------------------------------------------------------------------------
 // global pass bookkeeping
 // ---------------------------------------------------------------------------
+// Count-matrix layout of one segment: one row per gap class j (0..P) holding
+// its per-chunk counts, followed by ONE entry with the total of equality run j
+// (equality runs are filled, never scattered: only their sizes matter).  A flat
+// scan of the rows therefore yields, in class order, each gap chunk's
+// destination and each equality run's start.
+__host__ __device__ __forceinline__ long long mat_row(const Seg &g) { return (long long)g.nch + 1; }
+__host__ __device__ __forceinline__ long long mat_entries(const Seg &g) { return ((long long)g.P + 1) * mat_row(g); }
+__host__ __device__ __forceinline__ long long mat_gap(const Seg &g, int j, int chunk)
+{
+    return g.mat_off + (long long)j * mat_row(g) + chunk;
+}
+__host__ __device__ __forceinline__ long long mat_eq(const Seg &g, int j) { return g.mat_off + (long long)j * mat_row(g) + g.nch; }
+
 // One CTA: per-segment pass shape (P, rows, chunks, LUT size) and exclusive
 // scans over segments for pool offsets and the count-matrix layout; then an
 // L2 prefetch of this level's count matrix and offsets (they are written with
@@ -453,7 +466,7 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
         long long tp, tl, tm, tc;
         long long xp = block_exclusive_scan(in ? g.P + 1 : 0, sh, &tp);
         long long xl = block_exclusive_scan(in ? g.T : 0, sh, &tl);
-        long long xm = block_exclusive_scan(in ? (long long)g.rows * g.nch : 0, sh, &tm);
+        long long xm = block_exclusive_scan(in ? mat_entries(g) : 0, sh, &tm);
         long long xc = block_exclusive_scan(in ? g.nch : 0, sh, &tc);
         if (in) {
             g.piv_off = (int)(c_piv + xp);
@@ -498,7 +511,8 @@ struct PivotsSmem {
 constexpr int kPivotThreads = 1024;
 
 __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *nseg, const double *src,
-                                                          double *piv_pool, unsigned *lut_pool, int *chunk_seg)
+                                                          double *piv_pool, unsigned *lut_pool, int *chunk_seg,
+                                                          unsigned *mat)
 {
     KS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -517,6 +531,7 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *
         for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = piv[i];
         for (int t = threadIdx.x; t < T; t += blockDim.x) lut_pool[g.lut_off + t] = lut[t];
         for (int c = threadIdx.x; c < g.nch; c += blockDim.x) chunk_seg[g.ch_off + c] = s;
+        for (int q = threadIdx.x; q <= g.P; q += blockDim.x) mat[mat_eq(g, q)] = 0u;   // equality-run totals
         KS_TR(12);
         if (threadIdx.x == 0) {
             segs[s].k = k;
@@ -640,7 +655,10 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
             atomicAdd(&hist[classify(v, P.piv, P.lut, lo, scale, T)], 1u);
         }
         __syncthreads();
-        for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) mat[sg.mat_off + (long long)c * sg.nch + j] = hist[c];
+        for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) {
+            if (!(c & 1)) mat[mat_gap(sg, c >> 1, j)] = hist[c];
+            else if (hist[c]) atomicAdd(&mat[mat_eq(sg, c >> 1)], hist[c]);   // (zeroed by k_pivots)
+        }
     }
     if (kGate) gate_flush(bad, pz, nz, st);
 }
@@ -805,7 +823,8 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *
 // start of class c inside segment g (relative), c in [0, rows]; rows -> len
 __device__ __forceinline__ long long class_start(const Seg &g, const long long *moff, long long base_i, int c)
 {
-    return c < g.rows ? moff[g.mat_off + (long long)c * g.nch] - base_i : g.len;
+    if (c >= g.rows) return g.len;
+    return moff[(c & 1) ? mat_eq(g, c >> 1) : mat_gap(g, c >> 1, 0)] - base_i;
 }
 
 // ---------------------------------------------------------------------------
@@ -848,7 +867,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
         const long long base = g.start + (long long)j * kChunk;
         const int cnt = (int)min((long long)kChunk, g.len - (long long)j * kChunk);
         const long long base_i = moff[g.mat_off];
-        const int nch = g.nch, T = g.T;
+        const int T = g.T;
         const double lo = g.lo, scale = g.scale;
         double *out = dst + g.start;
         for (int q0 = 0; q0 <= g.k; q0 += 4 * blockDim.x) {   // 4 gaps per thread in flight
@@ -857,7 +876,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int q = q0 + u * blockDim.x + threadIdx.x;
-                const long long e = g.mat_off + (long long)(2 * q) * nch + j;
+                const long long e = mat_gap(g, q, j);
                 off[u] = q <= g.k ? moff[e] : base_i;
                 cnt[u] = q <= g.k ? mat[e] : 0u;
             }
@@ -1871,7 +1890,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
     L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
-    L.mat_cap = (2 * psum + L.seg_cap) + (long long)(2 * kPMax + 1) * (2 * (n / kChunk) + 2);
+    L.mat_cap = (psum + L.seg_cap) * 2 + (long long)(kPMax + 1) * (2 * (n / kChunk) + 4);
     // warp units and fill items of one leaf launch: disjoint final ranges of > kTinyGap keys
     L.unit_cap = (int)(2 * (n / (kTinyGap + 1)) + nseg0 + 4096);
     L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
@@ -2107,7 +2126,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         });
         K.run(kPhPivots, [&] {
             launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src, piv,
-                   lut, chunk_seg);
+                   lut, chunk_seg, mat);
         });
         if (level == 0)
             K.run(kPhCount, [&] {
