@@ -542,6 +542,116 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *
     }
 }
 
+// Level 0 of a single array (one segment, P up to 2047): the pivot build is on
+// the critical path while all other SMs idle, so it is spread over the GPU.
+// k_pivot_rank: each thread ranks one of the first P keys against all of them
+// (ties by position) and writes it to its sorted place; k_pivot_lut: every CTA
+// de-duplicates the sorted run and builds its slice of the bucket LUT.
+constexpr int kRankThreads = 128;
+constexpr int kRankParts = 8;   // threads per ranked key (a power of two dividing 32)
+
+__global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const Seg *segs, const double *src, double *sorted)
+{
+    KS_PDL_ENTRY();
+    __shared__ double x[kPMax + 1];
+    const Seg g = segs[0];
+    const int P = g.P;
+    const double *in = src + g.start;
+    constexpr int kU = (kPMax + 1 + kRankThreads - 1) / kRankThreads;   // all loads in flight at once
+    double t[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const int i = u * kRankThreads + threadIdx.x;
+        t[u] = i < P ? __ldcg(in + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+        const int i = u * kRankThreads + threadIdx.x;
+        if (i < P) x[i] = t[u];
+    }
+    __syncthreads();
+    // kRankParts threads per key, each counting over a slice of the P keys
+    const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = gt / kRankParts, part = gt % kRankParts;
+    const int per = (P + kRankParts - 1) / kRankParts;
+    const int j0 = part * per, j1 = min(P, j0 + per);
+    const double v = i < P ? x[i] : 0.0;
+    int r = 0;
+#pragma unroll 8
+    for (int j = j0; j < j1; ++j) {
+        const double y = x[j];
+        r += (y < v || (y == v && j < i)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = kRankParts / 2; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (i < P && part == 0) sorted[r] = v;   // (NaN keys -- rejected by the gate -- may collide; all in range)
+}
+
+constexpr int kLutCtas = 16;
+
+__global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const double *sorted, double *piv_pool,
+                                                             unsigned *lut_pool, int *chunk_seg, unsigned *mat)
+{
+    KS_PDL_ENTRY();
+    __shared__ double piv[kPMax + kPivPad];
+    __shared__ long long sh[33];
+    const Seg g = segs[0];
+    const int P = g.P;
+    long long carry = 0;
+    for (int base = 0; base < P; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const double v = i < P ? __ldcg(sorted + i) : 0.0;
+        const int keep = (i < P && (i == 0 || v != __ldcg(sorted + i - 1))) ? 1 : 0;
+        long long tot;
+        const long long pos = block_exclusive_scan(keep, sh, &tot);
+        if (keep) piv[carry + pos] = v;
+        carry += tot;
+    }
+    const int k = (int)carry;
+    if (threadIdx.x < kPivPad) piv[k + threadIdx.x] = CUDART_NAN;
+    __syncthreads();
+    // same transform as build_pivots
+    int T = g.T;
+    const double lo = piv[0], hi = piv[k - 1];
+    double scale = 0.0;
+    if (T > 1 && k >= 2 && hi > lo) {
+        scale = (double)T / (hi - lo);
+        if (!(scale > 0.0) || isinf(scale)) T = 1;
+    } else {
+        T = 1;
+    }
+    if (T == 1) scale = 0.0;
+    // this CTA's LUT slice: one bucket run per thread, a = #pivots in buckets < t
+    const int per_cta = (T + gridDim.x - 1) / gridDim.x;
+    const int c0 = blockIdx.x * per_cta, c1 = min(T, c0 + per_cta);
+    const int per = (c1 - c0 + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int t0 = c0 + threadIdx.x * per, t1 = min(c1, t0 + per);
+    if (t0 < t1) {
+        int a = 0, hi_i = k;
+        while (a < hi_i) {
+            const int mid = (a + hi_i) >> 1;
+            if (lut_bucket(piv[mid], lo, scale, T) < t0) a = mid + 1; else hi_i = mid;
+        }
+        for (int t = t0; t < t1; ++t) {
+            int b = a;
+            while (b < k && lut_bucket(piv[b], lo, scale, T) <= t) ++b;
+            lut_pool[g.lut_off + t] = lut_pack(a, b);
+            a = b;
+        }
+    }
+    if (blockIdx.x == 0) {
+        for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = piv[i];
+        for (int c = threadIdx.x; c < g.nch; c += blockDim.x) chunk_seg[g.ch_off + c] = 0;
+        for (int q = threadIdx.x; q <= g.P; q += blockDim.x) mat[mat_eq(g, q)] = 0u;   // equality-run totals
+        if (threadIdx.x == 0) {
+            segs[0].k = k;
+            segs[0].T = T;
+            segs[0].lo = lo;
+            segs[0].scale = scale;
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // count: per (segment, chunk) class histogram -> class-major count matrix
 // (shared-memory atomics: measured ~0.03 SM-cycles/key on B200, far cheaper
@@ -1072,7 +1182,10 @@ __device__ __forceinline__ void account_partition(DevStatus *st, long long len, 
 // ---------------------------------------------------------------------------
 // plan (global pass): class extents from the scanned count matrix
 // ---------------------------------------------------------------------------
-constexpr int kPlanThreads = 512;
+#ifndef KS_PLAN_THREADS
+#define KS_PLAN_THREADS 128
+#endif
+constexpr int kPlanThreads = KS_PLAN_THREADS;
 constexpr int kPlanChunks = (kPMax + 1 + kPlanThreads - 1) / kPlanThreads;   // grid.y: pivot-pair chunks
 
 // One CTA per (segment, chunk of kPlanThreads pivot pairs): gap 2j and
@@ -1863,15 +1976,13 @@ static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
 }
 
 // Small reset kernel (replaces memset nodes, which would break the PDL chain).
-__global__ void k_set_ints(int *p0, int *p1, int *p2, int *p3)
+struct IntPtrs {
+    int *p[8];
+};
+__global__ void k_set_ints(IntPtrs z)
 {
     KS_PDL_ENTRY();
-    if (threadIdx.x == 0) {
-        if (p0) *p0 = 0;
-        if (p1) *p1 = 0;
-        if (p2) *p2 = 0;
-        if (p3) *p3 = 0;
-    }
+    if (threadIdx.x < 8 && z.p[threadIdx.x]) *z.p[threadIdx.x] = 0;
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -2124,10 +2235,23 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
                    L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next);
         });
-        K.run(kPhPivots, [&] {
-            launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src, piv,
-                   lut, chunk_seg, mat);
-        });
+        if (level == 0 && d_off == nullptr) {   // one segment, known P: build the pivots GPU-wide
+            const int P0 = pivots_for(n, kPMax);
+            double *sorted = reinterpret_cast<double *>(moff);   // (scratch: the offsets are written later)
+            K.run(kPhPivots, [&] {
+                launch(k_pivot_rank, dim3((P0 * kRankParts + kRankThreads - 1) / kRankThreads), dim3(kRankThreads), 0,
+                       stream, segs[gcur], src, sorted);
+            });
+            K.run(kPhPivots, [&] {
+                launch(k_pivot_lut, dim3(kLutCtas), dim3(kPivotThreads), 0, stream, segs[gcur], sorted, piv, lut,
+                       chunk_seg, mat);
+            });
+        } else {
+            K.run(kPhPivots, [&] {
+                launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src,
+                       piv, lut, chunk_seg, mat);
+            });
+        }
         if (level == 0)
             K.run(kPhCount, [&] {
                 launch(k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
@@ -2164,7 +2288,9 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     auto leaf = [&]() {
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1};
         K.run(kPhLeaf, [&] { launch(k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head);
+        // queue claims reset before the small sorts (their hand-backs belong to the next epoch)
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream,
+               IntPtrs{{&st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head, nullptr, nullptr, nullptr, nullptr}});
         LeafQ Qn = Q;
         ++Qn.epoch;
         K.run(kPhLeaf, [&] {
@@ -2175,10 +2301,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             launch(k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
                    &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp);
         });
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nsmall[0], &st->nsmall[1], &st->small_next[0],
-               &st->small_next[1]);
         K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream, &st->nunits, (int *)nullptr, (int *)nullptr, (int *)nullptr);
+        launch(k_set_ints, dim3(1), dim3(32), 0, stream,
+               IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,
+                        nullptr, nullptr}});
         Q = Qn;
         ++leaves_run;
     };
