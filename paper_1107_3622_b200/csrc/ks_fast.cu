@@ -1075,7 +1075,7 @@ struct EmitArgs {
 
 // packed per-thread counts for one block scan (11 bits each; blocks <= 1024 threads):
 // units + fill items (<= 2 per thread), local items, global segments, sort items
-constexpr int kPkU = 0, kPkL = 11, kPkG = 22, kPkS = 33;
+constexpr int kPkU = 0, kPkL = 11, kPkG = 22, kPkS = 33, kPkLB = 44;
 __device__ __forceinline__ long long pk_get(long long x, int sh, int bits) { return (x >> sh) & ((1ll << bits) - 1); }
 
 // sort up to kTinyGap keys with one thread (src may equal dst)
@@ -1120,14 +1120,20 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         for (long long i = 0; i < el; ++i) A.keys[ae + i] = pv;
     const int f_eq = (have && el > kFillDirect) ? 1 : 0;
     const int nu = u_gap + f_eq;
+    // the plan stores big local items at the front of the local queue, the others from
+    // the back: the leaf launch takes them front to back (longest first)
+    const int lb_gap = (l_gap && !A.in_leaf && gl > kLocalBig) ? 1 : 0;
+    if (lb_gap) l_gap = 0;
     const long long pk = ((long long)nu << kPkU) | ((long long)l_gap << kPkL) | ((long long)g_gap << kPkG) |
-                         ((long long)s_gap << kPkS);
+                         ((long long)s_gap << kPkS) | ((long long)lb_gap << kPkLB);
     long long tpk;
     const long long xpk = block_exclusive_scan(pk, sh, &tpk);
     if (threadIdx.x == 0) {
         const int tu = (int)pk_get(tpk, kPkU, 11), tl = (int)pk_get(tpk, kPkL, 11);
         const int tg = (int)pk_get(tpk, kPkG, 11), ts = (int)pk_get(tpk, kPkS, 11);
-        if (tl + ts) atomicAdd(&st->pending, tl + ts);   // before the slots become claimable
+        const int tlb = (int)pk_get(tpk, kPkLB, 11);
+        if (tl + ts + tlb) atomicAdd(&st->pending, tl + ts + tlb);   // before the slots become claimable
+        sbase[4] = tlb ? atomicAdd(&st->lqb_claim, tlb) : 0;
         sbase[0] = tu ? atomicAdd(&st->nunits, tu) : 0;
         sbase[1] = tl ? atomicAdd(A.in_leaf ? &st->sq_claim : &st->lq_claim, tl) : 0;
         sbase[2] = tg ? atomicAdd(A.ngnext, tg) : 0;
@@ -1151,7 +1157,11 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         const int i = (int)(sbase[1] + pk_get(xpk, kPkL, 11));
         const Seg c = with_kind(make_seg(ag, gl, dst_id), kItemLocal);
         if (A.in_leaf) q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, i, c, A.Q.epoch);
-        else q_publish(A.Q.lq, A.Q.lq_ready, A.Q.lcap, i, c, A.Q.epoch);
+        else if (i < A.Q.lcap) A.Q.lq[A.Q.lcap - 1 - i] = c; else st->overflow = 7;   // (read after this launch)
+    }
+    if (lb_gap) {
+        const int i = (int)(sbase[4] + pk_get(xpk, kPkLB, 11));
+        if (i < A.Q.lcap) A.Q.lq[i] = with_kind(make_seg(ag, gl, dst_id), kItemLocal); else st->overflow = 7;
     }
     if (g_gap) {
         const long long gi = sbase[2] + pk_get(xpk, kPkG, 11);
@@ -1195,7 +1205,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
 {
     KS_PDL_ENTRY();
     __shared__ long long sh[33];
-    __shared__ long long sbase[4];
+    __shared__ long long sbase[5];
     if (abort_requested(st)) return;
     const int ns = *nseg;
     const int j0 = blockIdx.y * kPlanThreads;
@@ -1241,7 +1251,7 @@ struct LocalSmem {
     unsigned hist[kRowsMaxLocal + 1];
     unsigned cursor[kRowsMaxLocal + 1];
     long long sh[33];
-    long long sbase[4];
+    long long sbase[5];
 };
 
 // Partition one local segment (in global memory, L2-resident) with its first
@@ -1815,7 +1825,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
     long long tr_t0 = clock64();
 #endif
     // the plan's local items (all published before this launch): a fixed set
-    const int lq_n = *reinterpret_cast<volatile int *>(&st->lq_claim);
+    // (written by the plan, i.e. before this launch: big ones at the front, the rest at the back)
+    const int lq_nb = *reinterpret_cast<volatile int *>(&st->lqb_claim);
+    const int lq_n = lq_nb + *reinterpret_cast<volatile int *>(&st->lq_claim);
     bool local_phase = true;   // (thread 0 only)
     for (;;) {
         if (threadIdx.x == 0) {
@@ -1824,8 +1836,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
             if (local_phase) {
                 const int idx = atomicAdd(&st->lq_head, 1);
                 if (idx < lq_n) {
-                    const int slot = idx % Q.lcap;
-                    while (ld_acquire_u64(&Q.lq_ready[slot]) != q_tag(Q.epoch, idx)) __nanosleep(32);
+                    const int slot = idx < lq_nb ? idx : Q.lcap - 1 - (idx - lq_nb);
                     const Seg *q = Q.lq + slot;
                     ctl.seg = make_seg(__ldcg(&q->start), __ldcg(&q->len), __ldcg(&q->src));
                     kind = kItemLocal;
@@ -2290,7 +2301,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         K.run(kPhLeaf, [&] { launch(k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // queue claims reset before the small sorts (their hand-backs belong to the next epoch)
         launch(k_set_ints, dim3(1), dim3(32), 0, stream,
-               IntPtrs{{&st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head, nullptr, nullptr, nullptr, nullptr}});
+               IntPtrs{{&st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head, &st->lqb_claim, nullptr, nullptr,
+                        nullptr}});
         LeafQ Qn = Q;
         ++Qn.epoch;
         K.run(kPhLeaf, [&] {
@@ -2359,7 +2371,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     int rc = sync_status();
     if (rc != KS_OK) return rc;
     // remaining work (rare): more global levels, or hand-backs queued for another leaf launch
-    while (!aborted() && (h.nseg[gcur] > 0 || h.sq_claim > 0 || h.lq_claim > 0)) {
+    while (!aborted() && (h.nseg[gcur] > 0 || h.sq_claim > 0 || h.lq_claim > 0 || h.lqb_claim > 0)) {
         if (h.nseg[gcur] > 0) global_pass();
         leaf();
         rc = sync_status();

@@ -81,6 +81,7 @@ struct DevStatus {
     int nunits;                       // warp work items (unit sorts, fills) of the current pass
     // on-chip work queues of the leaf kernel (local partitions, segment sorts)
     int lq_claim, lq_head;            // local queue: slots claimed by producers / taken by consumers
+    int lqb_claim;                    // ... big local items (> kLocalBig), stored from the front (LPT)
     int sq_claim, sq_head;            // sort queue
     int pending;                      // queued or running leaf items (the leaf kernel ends at zero)
     int nsmall[2];                    // small-segment lists (size classes 0, 1), sorted after the leaf launch
