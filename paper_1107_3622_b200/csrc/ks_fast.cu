@@ -410,9 +410,9 @@ __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, un
     scale_out = scale;
 }
 
-__host__ __device__ __forceinline__ int pivots_for(long long len, int pmax)
+__host__ __device__ __forceinline__ int pivots_for(long long len, int pmax, int keys_per_pivot = kKeysPerPivot)
 {
-    long long P = cdiv(len, kKeysPerPivot);
+    long long P = cdiv(len, keys_per_pivot);
     if (P > pmax) P = pmax;
     if (P < 1) P = 1;
     return (int)P;
@@ -1265,7 +1265,7 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
     double *dst = (g.src ? keys : const_cast<double *>(tmp)) + g.start;
     const int dst_id = g.src ? 0 : 1;
     const int m = (int)g.len;
-    const int P = pivots_for(m, kPMaxLocal);
+    const int P = pivots_for(m, kPMaxLocal, kKeysPerPivotLocal);
     int k, T;
     double lo, scale;
     KS_TR_DECL;

@@ -28,6 +28,10 @@ constexpr int kPMaxLocal = 255;       // ... per local partition (P = len / kKey
 constexpr int kRowsMaxLocal = 2 * kPMaxLocal + 1;
 constexpr int kLutMaxLocal = 2048;
 constexpr int kKeysPerPivot = 2048;   // P = len / 2048 (capped): gaps land in the segment sorter's range
+#ifndef KS_LOCAL_KPP
+#define KS_LOCAL_KPP 2048
+#endif
+constexpr int kKeysPerPivotLocal = KS_LOCAL_KPP;   // local partitions (children mostly for the small sorts)
 constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
 constexpr int kCountThreads = 512;
 constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
