@@ -1441,6 +1441,7 @@ struct SortSmem {
     int big[kBigCap];
     double red[2][32];
     double bounds[2];      // lo, scale
+    int bits;              // bucket map in the order-preserving bit image (wide segments)
     unsigned sh[33];
     int nbig;
     int nmid;              // buckets of 5..kThreadSortMax keys (listed in the free `a` buffer)
@@ -1453,6 +1454,29 @@ __device__ __forceinline__ int sort_bucket(double v, double lo, double scale, in
     const int x = __double2int_rz((v - lo) * scale);
     return min(max(x, 0), B - 1);
 }
+
+// Order-preserving unsigned image of a double (sign-magnitude -> two's order).
+__device__ __forceinline__ unsigned long long ord_bits(double v)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Bucket map of the segment sorter: linear in the value, or -- when the
+// segment spans many binades (log-like data: linear buckets would overflow) --
+// linear in the order-preserving bit image.  Both are monotone in v.
+struct BucketMap {
+    double lo, scale;
+    unsigned long long ulo;
+    int bits;
+    int B;
+    __device__ __forceinline__ int operator()(double v) const
+    {
+        if (!bits) return sort_bucket(v, lo, scale, B);
+        const int x = __double2int_rz((double)(ord_bits(v) - ulo) * scale);
+        return min(max(x, 0), B - 1);
+    }
+};
 
 __device__ __forceinline__ void smem_insertion_sort(double *a, int s)
 {
@@ -1584,9 +1608,16 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
         if (lane == 0) {
             double scale = mx > mn ? (double)B / (mx - mn) : -1.0;            // -1: constant segment
-            if (mx > mn && (!(scale > 0.0) || isinf(scale))) scale = 0.0;    // range overflow / underflow
+            int bits = 0;
+            const bool wide = (mn > 0.0 && mx > 64.0 * mn) || (mx < 0.0 && mn < 64.0 * mx);
+            if (mx > mn && (wide || !(scale > 0.0) || isinf(scale))) {
+                bits = 1;   // many binades, or a range the linear map cannot hold
+                scale = (double)B / (double)(ord_bits(mx) - ord_bits(mn));
+                if (!(scale > 0.0) || isinf(scale)) scale = 0.0;
+            }
             S.bounds[0] = mn;
             S.bounds[1] = scale;
+            S.bits = bits;
         }
     }
     __syncthreads();
@@ -1600,9 +1631,10 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
     } else {
         if (scale == 0.0) B = 1;   // one bucket: the warp path (or the partitioner) takes it
+        const BucketMap bmap{lo, scale, ord_bits(lo), S.bits, B};
         // 2. bucket histogram, scan, scatter a -> b
 #pragma unroll 1
-        for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[sort_bucket(S.a[i], lo, scale, B)], 1u);
+        for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[bmap(S.a[i])], 1u);
         __syncthreads();
         KS_TRS(1);   // histogram
         {
@@ -1632,7 +1664,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 #pragma unroll 1
         for (int i = tid; i < m; i += kT) {
             const double x = S.a[i];
-            S.b[atomicAdd(&S.cur[sort_bucket(x, lo, scale, B)], 1u)] = x;
+            S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x;
         }
         __syncthreads();
         KS_TRS(2);   // scan + scatter
@@ -1657,7 +1689,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 #pragma unroll 1
         for (int i = tid; i < m; i += kT) {
             const double x = S.b[i];
-            const int bk = sort_bucket(x, lo, scale, B);
+            const int bk = bmap(x);
             const int e = (int)S.cur[bk];
             const int s0 = bk ? (int)S.cur[bk - 1] : 0;
             int pos = i;
