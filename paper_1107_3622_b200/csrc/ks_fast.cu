@@ -358,15 +358,9 @@ __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, un
     if (threadIdx.x < kPivPad) piv[k + threadIdx.x] = CUDART_NAN;
     __syncthreads();
     int T = Treq;
-    const double lo = piv[0], hi = piv[k - 1];
-    double scale = 0.0;
-    if (T > 1 && k >= 2 && hi > lo) {
-        scale = (double)T / (hi - lo);
-        if (!(scale > 0.0) || isinf(scale)) T = 1;
-    } else {
-        T = 1;
-    }
-    if (T == 1) scale = 0.0;
+    const double lo = piv[0];
+    double scale;
+    lut_transform(piv, k, T, scale);
     for (int t = threadIdx.x; t < T; t += blockDim.x) lut[t] = 0u;
     __syncthreads();
     for (int j = threadIdx.x; j < k; j += blockDim.x) atomicAdd(&lut[lut_bucket(piv[j], lo, scale, T)], 1u);
@@ -612,15 +606,9 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
     __syncthreads();
     // same transform as build_pivots
     int T = g.T;
-    const double lo = piv[0], hi = piv[k - 1];
-    double scale = 0.0;
-    if (T > 1 && k >= 2 && hi > lo) {
-        scale = (double)T / (hi - lo);
-        if (!(scale > 0.0) || isinf(scale)) T = 1;
-    } else {
-        T = 1;
-    }
-    if (T == 1) scale = 0.0;
+    const double lo = piv[0];
+    double scale;
+    lut_transform(piv, k, T, scale);
     // this CTA's LUT slice: one bucket run per thread, a = #pivots in buckets < t
     const int per_cta = (T + gridDim.x - 1) / gridDim.x;
     const int c0 = blockIdx.x * per_cta, c1 = min(T, c0 + per_cta);
@@ -1453,13 +1441,6 @@ __device__ __forceinline__ int sort_bucket(double v, double lo, double scale, in
 {
     const int x = __double2int_rz((v - lo) * scale);
     return min(max(x, 0), B - 1);
-}
-
-// Order-preserving unsigned image of a double (sign-magnitude -> two's order).
-__device__ __forceinline__ unsigned long long ord_bits(double v)
-{
-    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
-    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
 // Bucket map of the segment sorter: linear in the value, or -- when the

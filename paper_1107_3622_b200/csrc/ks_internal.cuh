@@ -152,11 +152,56 @@ __device__ __forceinline__ bool abort_requested(const DevStatus *st)
 // round monotonically, the float->int conversion saturates (and maps NaN to 0),
 // and scale is finite and > 0 whenever T > 1 (guarded where the table is
 // built), so the bucket map is monotone on every finite key.
+// Order-preserving unsigned image of a double (sign-magnitude -> two's order).
+__device__ __forceinline__ unsigned long long ord_bits(double v)
+{
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// scale < 0 selects the bit-image map: t = (ord(v) - ord(lo)) * |scale|, used
+// when the pivots are spread far more evenly in their bit image than in value
+// (log-like data: a linear map would crowd them into a few buckets).  Both
+// maps are monotone; keys below lo map to bucket 0.
 __device__ __forceinline__ int lut_bucket(double v, double lo, double scale, int T)
 {
     if (T <= 1) return 0;
-    const int x = __double2int_rz((v - lo) * scale);
+    double t;
+    if (scale >= 0.0) {
+        t = (v - lo) * scale;
+    } else {
+        const unsigned long long ov = ord_bits(v), ol = ord_bits(lo);
+        t = ov >= ol ? (double)(ov - ol) * -scale : -1.0;
+    }
+    const int x = __double2int_rz(t);
     return min(max(x, 0), T - 1);
+}
+
+// LUT transform for sorted distinct pivots piv[0..k): T buckets, linear or
+// bit-image (negative scale), whichever places the pivots' quartiles closer
+// to the buckets' quartiles; T = 1 (plain binary search) when no map works.
+__device__ __forceinline__ void lut_transform(const double *piv, int k, int &T, double &scale)
+{
+    scale = 0.0;
+    const double lo = piv[0], hi = piv[k > 0 ? k - 1 : 0];
+    if (!(T > 1 && k >= 2 && hi > lo)) {
+        T = 1;
+        return;
+    }
+    const double sl = (double)T / (hi - lo);
+    const double sb = (double)T / (double)(ord_bits(hi) - ord_bits(lo));
+    const bool lin_ok = sl > 0.0 && !isinf(sl), bit_ok = sb > 0.0 && !isinf(sb);
+    double err_l = 0.0, err_b = 0.0;
+    const double span_b = (double)(ord_bits(hi) - ord_bits(lo));
+    for (int q = 1; q <= 3; ++q) {
+        const double x = piv[(k - 1) * q / 4];
+        const double want = 0.25 * q;
+        err_l += fabs((x - lo) / (hi - lo) - want);
+        err_b += fabs((double)(ord_bits(x) - ord_bits(lo)) / span_b - want);
+    }
+    if (lin_ok && (!bit_ok || err_l <= err_b + 0.05)) scale = sl;   // (ties favour the linear map)
+    else if (bit_ok) scale = -sb;
+    else T = 1;
 }
 
 constexpr int kPivPad = 4;   // NaN slots after the k pivots (branch-free probes read up to piv[a+3])
