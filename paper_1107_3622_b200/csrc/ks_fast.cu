@@ -67,6 +67,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_GRAPH
 #define KS_GRAPH 1        // replay the speculative schedule as a cached CUDA graph
 #endif
+#ifndef KS_MINB1
+#define KS_MINB1 2        // resident CTAs per SM asked for the 512-thread small-segment sorter
+#endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
 #endif
@@ -1759,7 +1762,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 // shape pull them from a counter after the leaf launch.  Hand-backs go to the
 // next leaf launch's queue.
 template <int C>
-__global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? 2 : 5)
+__global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_MINB1 : 5)
     k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp)
 {
     KS_PDL_ENTRY();

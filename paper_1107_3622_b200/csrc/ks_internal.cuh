@@ -57,10 +57,13 @@ constexpr int kSortMax = 12288;
 #ifndef KS_LAM1
 #define KS_LAM1 2
 #endif
-__host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? 2048 : (c == 1 ? 6144 : kSortMax); }
+#ifndef KS_CAP1
+#define KS_CAP1 6144
+#endif
+__host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? 2048 : (c == 1 ? KS_CAP1 : kSortMax); }
 __host__ __device__ constexpr int sort_threads(int c) { return c == 0 ? KS_T0 : (c == 1 ? 512 : 1024); }
 __host__ __device__ constexpr int sort_lambda(int c) { return c == 0 ? KS_LAM0 : (c == 1 ? KS_LAM1 : 2); }   // keys per bucket
-__host__ __device__ __forceinline__ int sort_class(long long len) { return len <= 2048 ? 0 : (len <= 6144 ? 1 : 2); }
+__host__ __device__ __forceinline__ int sort_class(long long len) { return len <= sort_cap(0) ? 0 : (len <= sort_cap(1) ? 1 : 2); }
 constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
 #ifndef KS_LOCAL_THREADS
 #define KS_LOCAL_THREADS 1024
