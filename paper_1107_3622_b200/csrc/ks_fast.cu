@@ -2316,9 +2316,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1};
         K.run(kPhLeaf, [&] { launch(k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // queue claims reset before the small sorts (their hand-backs belong to the next epoch)
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream,
-               IntPtrs{{&st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head, &st->lqb_claim, nullptr, nullptr,
-                        nullptr}});
+        K.run(kPhGate, [&] {   // (bookkeeping launches are booked under "gate")
+            launch(k_set_ints, dim3(1), dim3(32), 0, stream,
+                   IntPtrs{{&st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head, &st->lqb_claim, nullptr, nullptr,
+                            nullptr}});
+        });
         LeafQ Qn = Q;
         ++Qn.epoch;
         K.run(kPhLeaf, [&] {
@@ -2330,9 +2332,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                    &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp);
         });
         K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
-        launch(k_set_ints, dim3(1), dim3(32), 0, stream,
-               IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,
-                        nullptr, nullptr}});
+        K.run(kPhGate, [&] {
+            launch(k_set_ints, dim3(1), dim3(32), 0, stream,
+                   IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,
+                            nullptr, nullptr}});
+        });
         Q = Qn;
         ++leaves_run;
     };
