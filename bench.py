@@ -147,6 +147,29 @@ def dist_setup(want_nccl: bool):
 # reference arm: the reference's K-sort on host cores
 # ---------------------------------------------------------------------------
 
+def replica_seed(rank: int) -> int:
+    """Rank r sorts its own array: the reference generator's per-replication
+    seed convention (derive_seed, bench.py:147 of the reference)."""
+    if rank == 0:
+        return SEED
+    from oracle import oracle as O  # seed derivation only (pure arithmetic)
+    return O.derive_seed(SEED, rank, 0)
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    """The slowest rank's time (the job's time): all-reduce MAX."""
+    import torch
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_value(world: int, n: int, steps: int, max_ms: float) -> float:
+    """Whole-job keys/s: every rank sorted `steps` arrays of n keys."""
+    return world * n * steps / (max_ms * 1e-3)
+
+
 def run_reference(args):
     rank, world, _ = dist_setup(want_nccl=False)
     if rank != 0:
@@ -234,10 +257,7 @@ def run_ours(args):
     from paper_1107_3622_b200.sort_core import _sort_device, _stream_ptr, _workspace
 
     n = args.n
-    seed = SEED if rank == 0 else None
-    if seed is None:
-        from oracle import oracle as O  # seed derivation only (pure arithmetic)
-        seed = O.derive_seed(SEED, rank, 0)
+    seed = replica_seed(rank)
     pristine = K.generate_device(n, seed, args.kind)
     keys = torch.empty_like(pristine)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
@@ -274,10 +294,7 @@ def run_ours(args):
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     my_ms = sum(step_ms)
-    t = torch.tensor([my_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-    max_ms = float(t.item())
+    max_ms = max_over_ranks(my_ms, world, "cuda")
     stats = K.last_stats
     # correctness of the last timed output: sorted and a permutation (checksum of bits)
     ok = bool(K.is_sorted(keys))
@@ -314,7 +331,7 @@ def run_ours(args):
 
     if rank != 0:
         return
-    value = world * n * args.steps / (max_ms * 1e-3)
+    value = job_value(world, n, args.steps, max_ms)
     ms_per_step = max_ms / args.steps
     multi_pass_gbs = stats.bytes_moved / (ms_per_step * 1e-3) / 1e9
     line = {
