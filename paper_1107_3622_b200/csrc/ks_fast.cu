@@ -938,6 +938,22 @@ __device__ __forceinline__ long long class_start(const Seg &g, const long long *
 // runs (odd classes) are not written: the finish pass fills them, so only
 // gap classes carry a cursor.
 // ---------------------------------------------------------------------------
+#ifndef KS_ST_HINT
+#define KS_ST_HINT 0      // cache hint of the scattered stores (0 default, 1 .cg, 2 .cs, 3 .wt)
+#endif
+__device__ __forceinline__ void scatter_store(double *p, double v)
+{
+#if KS_ST_HINT == 1
+    __stcg(p, v);
+#elif KS_ST_HINT == 2
+    __stcs(p, v);
+#elif KS_ST_HINT == 3
+    __stwt(p, v);
+#else
+    *p = v;
+#endif
+}
+
 struct ScatterSmem {
     PassSmem P;
     unsigned cursor[kPMax + 1];   // next slot per gap class, relative to the segment start
@@ -990,7 +1006,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
 #if KS_PREFETCH
                     // pull this chunk's destination run of gap q into L2 ahead of the
                     // 8-byte stores (a partial-sector store that misses L2 waits for a fill)
-                    l2_prefetch(out + c0, 8ull * cnt[u]);
+                    l2_prefetch_lines(out + c0, 8ull * cnt[u]);
 #endif
                 }
             }
@@ -1025,7 +1041,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
 #elif KS_SCATTER_EXP == 3   // experiment: slots taken, scattered stores of L2-resident lines (wrong output)
                 if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u) & 0x3fffff] = v[u];
 #else
-                if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u)] = v[u];
+                if (!(c & 1)) scatter_store(out + atomicAdd(&S.cursor[c >> 1], 1u), v[u]);
 #endif
             }
 #endif
@@ -1033,7 +1049,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
         for (int i = i0 + threadIdx.x; i < cnt; i += kPassThreads) {
             const double v = src[base + i];
             const int c = classify(v, S.P.piv, S.P.lut, lo, scale, T);
-            if (!(c & 1)) out[atomicAdd(&S.cursor[c >> 1], 1u)] = v;
+            if (!(c & 1)) scatter_store(out + atomicAdd(&S.cursor[c >> 1], 1u), v);
         }
     }
 }

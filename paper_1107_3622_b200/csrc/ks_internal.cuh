@@ -296,6 +296,18 @@ __device__ __forceinline__ void l2_prefetch(const void *p, unsigned long long by
     }
 }
 
+// Per-thread L2 prefetch of the 128-byte lines covering [p, p + bytes): a plain
+// (non-uniform) instruction per line, for many small ranges at once -- the
+// bulk form takes a uniform operand and serialises across the lanes of a warp.
+__device__ __forceinline__ void l2_prefetch_lines(const void *p, unsigned long long bytes)
+{
+    if (bytes == 0) return;
+    const unsigned long long a0 = reinterpret_cast<unsigned long long>(p) & ~127ull;
+    const unsigned long long a1 = reinterpret_cast<unsigned long long>(p) + bytes;
+    for (unsigned long long a = a0; a < a1; a += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a) : "memory");
+}
+
 __host__ __device__ __forceinline__ long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
 __host__ __device__ __forceinline__ int next_pow2(int x)
