@@ -1082,7 +1082,8 @@ struct EmitArgs {
 
 // packed per-thread counts for one block scan (11 bits each; blocks <= 1024 threads):
 // units + fill items (<= 2 per thread), local items, global segments, sort items
-constexpr int kPkU = 0, kPkL = 11, kPkG = 22, kPkS = 33, kPkLB = 44;
+constexpr int kPkU = 0, kPkL = 16, kPkG = 27, kPkS = 38, kPkLB = 49;   // (units: 16 bits)
+constexpr int kFillPiece = 4096;   // long fills are split so that many warps write them
 __device__ __forceinline__ long long pk_get(long long x, int sh, int bits) { return (x >> sh) & ((1ll << bits) - 1); }
 
 // sort up to kTinyGap keys with one thread (src may equal dst)
@@ -1125,7 +1126,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     }
     if (have && el > 0 && el <= kFillDirect)
         for (long long i = 0; i < el; ++i) A.keys[ae + i] = pv;
-    const int f_eq = (have && el > kFillDirect) ? 1 : 0;
+    const int f_eq = (have && el > kFillDirect) ? (int)((el + kFillPiece - 1) / kFillPiece) : 0;   // fill pieces
     const int nu = u_gap + f_eq;
     // the plan stores big local items at the front of the local queue, the others from
     // the back: the leaf launch takes them front to back (longest first)
@@ -1136,7 +1137,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     long long tpk;
     const long long xpk = block_exclusive_scan(pk, sh, &tpk);
     if (threadIdx.x == 0) {
-        const int tu = (int)pk_get(tpk, kPkU, 11), tl = (int)pk_get(tpk, kPkL, 11);
+        const int tu = (int)pk_get(tpk, kPkU, 16), tl = (int)pk_get(tpk, kPkL, 11);
         const int tg = (int)pk_get(tpk, kPkG, 11), ts = (int)pk_get(tpk, kPkS, 11);
         const int tlb = (int)pk_get(tpk, kPkLB, 11);
         if (tl + ts + tlb) atomicAdd(&st->pending, tl + ts + tlb);   // before the slots become claimable
@@ -1147,13 +1148,14 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         sbase[3] = ts ? atomicAdd(&st->sq_claim, ts) : 0;
     }
     __syncthreads();
-    long long ui = sbase[0] + pk_get(xpk, kPkU, 11);
+    long long ui = sbase[0] + pk_get(xpk, kPkU, 16);
     if (u_gap) {
         if (ui < A.ucap) A.units[ui] = make_item(ag, gl, kItemUnit, dst_id); else st->overflow = 3;
         ++ui;
     }
-    if (f_eq) {
-        Item it = make_item(ae, el, kItemFill, dst_id);
+    for (int f = 0; f < f_eq; ++f, ++ui) {   // fill pieces of <= kFillPiece keys
+        const long long off = (long long)f * kFillPiece;
+        Item it = make_item(ae + off, min((long long)kFillPiece, el - off), kItemFill, dst_id);
         it.value = pv;
         if (ui < A.ucap) A.units[ui] = it; else st->overflow = 3;
     }
@@ -1180,7 +1182,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     EmitOut o;
     o.unit_keys = tk >> 32;
     o.fill_keys = tk & 0xffffffffll;
-    o.items = pk_get(tpk, kPkU, 11);
+    o.items = pk_get(tpk, kPkU, 16);
     return o;
 }
 
@@ -1378,46 +1380,39 @@ __device__ __forceinline__ void warp_unit_sort(const double *__restrict__ in, do
     __syncwarp();
 }
 
-__global__ void __launch_bounds__(kUnitWarps * 32, 3) k_finish_units(const Item *units, const DevStatus *cst,
-                                                                     double *keys, const double *tmp)
+// One finishing item by one warp: a fill, or a unit (<= kUnitMax keys) sorted
+// in registers through the warp's shared slice `sm` (sidx_size(kUnitMax) doubles).
+__device__ void finish_item(const Item &it, double *keys, const double *tmp, double *sm)
 {
-    KS_PDL_ENTRY();
-    __shared__ double sm_all[kUnitWarps][sidx_size(kUnitMax)];
-    if (abort_requested(cst)) return;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    double *sm = sm_all[wid];
-    const int n = cst->nunits;
-    for (int d = blockIdx.x * kUnitWarps + wid; d < n; d += gridDim.x * kUnitWarps) {
-        const Item it = units[d];
-        double *out = keys + it.start;
-        const int m = it.len;
-        if (it.kind == kItemFill) {
-            for (int i = lane; i < m; i += 32) out[i] = it.value;
-            continue;
-        }
-        const double *in = (it.src ? tmp : keys) + it.start;
-        if (m <= 2) {
-            if (lane == 0) {
-                const double a = in[0];
-                if (m == 2) {
-                    const double b = in[1];
-                    out[0] = b < a ? b : a;
-                    out[1] = b < a ? a : b;
-                } else {
-                    out[0] = a;
-                }
+    const int lane = threadIdx.x & 31;
+    double *out = keys + it.start;
+    const int m = it.len;
+    if (it.kind == kItemFill) {
+        for (int i = lane; i < m; i += 32) out[i] = it.value;
+        return;
+    }
+    const double *in = (it.src ? tmp : keys) + it.start;
+    if (m <= 2) {
+        if (lane == 0) {
+            const double a = in[0];
+            if (m == 2) {
+                const double b = in[1];
+                out[0] = b < a ? b : a;
+                out[1] = b < a ? a : b;
+            } else {
+                out[0] = a;
             }
-        } else if (m <= 32) {
-            warp_unit_sort<1>(in, out, m, sm);
-        } else if (m <= 64) {
-            warp_unit_sort<2>(in, out, m, sm);
-        } else if (m <= 128) {
-            warp_unit_sort<4>(in, out, m, sm);
-        } else if (m <= 256) {
-            warp_unit_sort<8>(in, out, m, sm);
-        } else {
-            warp_unit_sort<16>(in, out, m, sm);
         }
+    } else if (m <= 32) {
+        warp_unit_sort<1>(in, out, m, sm);
+    } else if (m <= 64) {
+        warp_unit_sort<2>(in, out, m, sm);
+    } else if (m <= 128) {
+        warp_unit_sort<4>(in, out, m, sm);
+    } else if (m <= 256) {
+        warp_unit_sort<8>(in, out, m, sm);
+    } else {
+        warp_unit_sort<16>(in, out, m, sm);
     }
 }
 
@@ -1779,7 +1774,8 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 // next leaf launch's queue.
 template <int C>
 __global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_MINB1 : 5)
-    k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp)
+    k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp,
+              const Item *units)
 {
     KS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1823,6 +1819,14 @@ __global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_M
         add_bytes(st, kPhLeaf, 16ull * keys_sorted);
         atomicAdd(&st->keys_leaf, keys_sorted);
         atomicAdd(&st->leaves, segs_sorted);
+    }
+    if (C == 0) {   // the last kernel of the launch also finishes the warp units and fills
+        constexpr int kW = sort_threads(C) / 32;
+        static_assert(kW * sidx_size(kUnitMax) <= 2 * SortSmem<C>::kCap, "unit scratch fits the a + b buffers");
+        __syncthreads();
+        double *sm = S.a + (threadIdx.x >> 5) * sidx_size(kUnitMax);   // (a and b are contiguous)
+        const int nu = st->nunits;
+        for (int d = blockIdx.x * kW + (threadIdx.x >> 5); d < nu; d += gridDim.x * kW) finish_item(units[d], keys, tmp, sm);
     }
 }
 
@@ -2046,7 +2050,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
     L.mat_cap = (psum + L.seg_cap) * 2 + (long long)(kPMax + 1) * (2 * (n / kChunk) + 4);
     // warp units and fill items of one leaf launch: disjoint final ranges of > kTinyGap keys
-    L.unit_cap = (int)(2 * (n / (kTinyGap + 1)) + nseg0 + 4096);
+    L.unit_cap = (int)(2 * (n / (kTinyGap + 1)) + n / kFillPiece + nseg0 + 4096);
     L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
     size_t off = 0;
     L.o_status = off; off = align_up(off + sizeof(DevStatus));
@@ -2073,7 +2077,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 // Per-device launch shapes and kernel attributes, set up once per process
 // (cudaFuncSetAttribute / occupancy queries cost host time on every call).
 struct EngineCfg {
-    int sms, g_count, g_scatter, g_units, g_leaf, g_small[2];
+    int sms, g_count, g_scatter, g_leaf, g_small[2];
 };
 
 static const EngineCfg *engine_cfg()
@@ -2109,7 +2113,6 @@ static const EngineCfg *engine_cfg()
     };
     c.g_count = grid(k_count<false>, kCountThreads, sizeof(CountSmem));
     c.g_scatter = grid(k_scatter, kPassThreads, sizeof(ScatterSmem));
-    c.g_units = grid(k_finish_units, kUnitWarps * 32, 0);
     c.g_leaf = grid(k_leaf, kLeafThreads, kLeafSmem);
     c.g_small[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
     c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
@@ -2226,7 +2229,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const EngineCfg *cfg = engine_cfg();
     if (cfg == nullptr) return KS_CUDA_ERROR;
     const int sms = cfg->sms;
-    const int g_count = cfg->g_count, g_scatter = cfg->g_scatter, g_units = cfg->g_units, g_leaf = cfg->g_leaf;
+    const int g_count = cfg->g_count, g_scatter = cfg->g_scatter, g_leaf = cfg->g_leaf;
     const int g_scan = sms * 2;
     const int g_pivots = sms;
     Launcher K(stream, profile);
@@ -2341,13 +2344,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         ++Qn.epoch;
         K.run(kPhLeaf, [&] {
             launch(k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, Q.small[1],
-                   &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp);
+                   &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
         });
         K.run(kPhLeaf, [&] {
             launch(k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
-                   &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp);
+                   &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
         });
-        K.run(kPhLeaf, [&] { launch(k_finish_units, dim3(g_units), dim3(kUnitWarps * 32), 0, stream, units, st, keys, tmp); });
         K.run(kPhGate, [&] {
             launch(k_set_ints, dim3(1), dim3(32), 0, stream,
                    IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,
