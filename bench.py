@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--kind", choices=["uniform01", "dup256"], default="uniform01")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-vendor", action="store_true", help="skip the torch.sort context timing")
     return p.parse_args()
 
 
@@ -309,6 +310,25 @@ def run_ours(args):
     hbm, peak_kind = peaks()
     dom_gbs = phase[dom]["bytes"] / (phase[dom]["ms"] * 1e-3) / 1e9 if phase[dom]["ms"] > 0 else 0.0
 
+    # vendor context: torch.sort (a library radix sort carrying
+    # int64 indices) on the same device-resident input; reported, never called
+    # by the product
+    vendor = None
+    if not args.no_vendor:
+        v_ms = []
+        for i in range(6):
+            prep()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            torch.sort(keys)
+            b.record(stream)
+            torch.cuda.synchronize()
+            if i > 0:
+                v_ms.append(a.elapsed_time(b))
+        vms = statistics.median(v_ms)
+        vendor = {"impl": "torch.sort (values + int64 indices)", "ms": vms, "value": n / (vms * 1e-3),
+                  "unit": "keys/s"}
+
     # end to end through the public API on a pinned HOST tensor
     e2e = None
     if not args.no_e2e:
@@ -357,6 +377,7 @@ def run_ours(args):
         "step_ms": step_ms,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "vendor_context": vendor,
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(n, args.kind)

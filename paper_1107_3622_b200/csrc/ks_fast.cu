@@ -17,6 +17,7 @@
 // scatter -> plan; then local partition rounds (one CTA per segment) and one
 // warp-per-unit finishing launch.  No key crosses to the host; the host reads
 // one small status block per pass to decide whether another pass is needed.
+#include <algorithm>
 #include <cfloat>
 #include <cstdio>
 #include <mutex>
@@ -60,6 +61,9 @@ __device__ unsigned long long g_trace[32];
 #endif
 #ifndef KS_PDL
 #define KS_PDL 1          // programmatic dependent launch between the engine's kernels
+#endif
+#ifndef KS_PDL_HEAVY
+#define KS_PDL_HEAVY 0    // PDL also into the persistent grids (count, scatter, leaf, segment sorts)
 #endif
 #ifndef KS_RANK_LEAF
 #define KS_RANK_LEAF 0    // 1: in-bucket ranks per key instead of per-bucket networks
@@ -443,11 +447,22 @@ __host__ __device__ __forceinline__ long long mat_eq(const Seg &g, int j) { retu
 // scattered 4- and 8-byte stores).
 __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long long mat_cap, int ch_cap,
                               int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
-                              unsigned long long *tstat, int *nseg_next)
+                              unsigned long long *tstat, int *nseg_next, int items)
 {
     KS_PDL_ENTRY();
     __shared__ long long sh[33];
     int ns = *nseg;
+    // chunk size of this pass (see kChunk)
+    long long total = 0;
+    for (int base = 0; base < ns; base += blockDim.x) {
+        const int s = base + threadIdx.x;
+        long long t;
+        block_exclusive_scan(s < ns ? segs[s].len : 0ll, sh, &t);
+        total += t;
+    }
+    long long chunk = cdiv(cdiv(total, (long long)min(items, kChunkItemsMax)), (long long)kChunkAlign) * kChunkAlign;
+    if (ns > 1 && chunk > kChunk) chunk = kChunk;
+    if (chunk < kChunkMin) chunk = kChunkMin;
     long long c_piv = 0, c_lut = 0, c_mat = 0, c_ch = 0;
     for (int base = 0; base < ns; base += blockDim.x) {
         int s = base + threadIdx.x;
@@ -456,7 +471,7 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
             g = segs[s];
             g.P = pivots_for(g.len, kPMax);
             g.rows = 2 * g.P + 1;
-            g.nch = (int)cdiv(g.len, kChunk);
+            g.nch = (int)cdiv(g.len, chunk);
             g.T = lut_for(g.P, kLutMax);
         }
         const bool in = s < ns;
@@ -479,6 +494,7 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
     }
     if (threadIdx.x == 0) {
         st->nchunks = (int)c_ch;
+        st->chunk = (int)chunk;
         st->mat_total = c_mat;
         add_bytes(st, kPhScan, 16ull * (unsigned long long)c_mat);   // reduce 4B + apply 4B in, 8B out
         add_bytes(st, kPhPivots, 8ull * (unsigned long long)c_piv);  // first P keys of each segment
@@ -710,7 +726,7 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
     int cached = -1;
     long long bad = LLONG_MAX;
     unsigned pz = 0, nz = 0;
-    const int nchunks = cst->nchunks;
+    const int nchunks = cst->nchunks, chunk = cst->chunk;
     for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
         const int s = chunk_seg[ch];
         __syncthreads();
@@ -721,8 +737,8 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
         for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) hist[c] = 0;
         __syncthreads();
         const int j = ch - sg.ch_off;
-        const long long base = sg.start + (long long)j * kChunk;
-        const int cnt = (int)min((long long)kChunk, sg.len - (long long)j * kChunk);
+        const long long base = sg.start + (long long)j * chunk;
+        const int cnt = (int)min((long long)chunk, sg.len - (long long)j * chunk);
         const int T = sg.T;
         const double lo = sg.lo, scale = sg.scale;
         const double *in = src + base + threadIdx.x;
@@ -750,10 +766,21 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
             for (int u = 0; u < U; ++u) atomicAdd(&hist[classify(v[u], P.piv, P.lut, lo, scale, T)], 1u);
 #endif
         }
-        for (int i = i0 + threadIdx.x; i < cnt; i += kCountThreads) {
-            const double v = src[base + i];
-            if (kGate) gate_one(v, base + i, bad, pz, nz);
-            atomicAdd(&hist[classify(v, P.piv, P.lut, lo, scale, T)], 1u);
+        if (i0 < cnt) {   // the last partial block, loads still batched
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kCountThreads + threadIdx.x;
+                v[u] = i < cnt ? src[base + i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kCountThreads + threadIdx.x;
+                if (i < cnt) {
+                    if (kGate) gate_one(v[u], base + i, bad, pz, nz);
+                    atomicAdd(&hist[classify(v[u], P.piv, P.lut, lo, scale, T)], 1u);
+                }
+            }
         }
         __syncthreads();
         for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) {
@@ -971,7 +998,7 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
     constexpr int U = 8;
     if (abort_requested(cst)) return;   // non-finite key or both signed zeros: write nothing
     int cached = -1;
-    const int nchunks = cst->nchunks;
+    const int nchunks = cst->nchunks, chunk = cst->chunk;
     for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
         const int s = chunk_seg[ch];
         __syncthreads();
@@ -981,8 +1008,8 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
         }
         const Seg &g = S.sg;
         const int j = ch - g.ch_off;
-        const long long base = g.start + (long long)j * kChunk;
-        const int cnt = (int)min((long long)kChunk, g.len - (long long)j * kChunk);
+        const long long base = g.start + (long long)j * chunk;
+        const int cnt = (int)min((long long)chunk, g.len - (long long)j * chunk);
         const long long base_i = moff[g.mat_off];
         const int T = g.T;
         const double lo = g.lo, scale = g.scale;
@@ -1046,10 +1073,21 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
             }
 #endif
         }
-        for (int i = i0 + threadIdx.x; i < cnt; i += kPassThreads) {
-            const double v = src[base + i];
-            const int c = classify(v, S.P.piv, S.P.lut, lo, scale, T);
-            if (!(c & 1)) scatter_store(out + atomicAdd(&S.cursor[c >> 1], 1u), v);
+        if (i0 < cnt) {   // the last partial block, loads still batched
+            double v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kPassThreads + threadIdx.x;
+                v[u] = i < cnt ? src[base + i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int i = i0 + u * kPassThreads + threadIdx.x;
+                if (i < cnt) {
+                    const int c = classify(v[u], S.P.piv, S.P.lut, lo, scale, T);
+                    if (!(c & 1)) scatter_store(out + atomicAdd(&S.cursor[c >> 1], 1u), v[u]);
+                }
+            }
         }
     }
 }
@@ -2005,9 +2043,10 @@ class Launcher {
 // Launch with programmatic stream serialization (PDL): the kernel may be
 // scheduled while its predecessor runs; KS_PDL_ENTRY() in every kernel waits
 // for the predecessor's completion before touching its results.
+constexpr bool kPdlHeavy = KS_PDL_HEAVY != 0;
 template <typename... KArgs, typename... Args>
-static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
-                          Args &&...args)
+static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, Args &&...args)
 {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -2016,10 +2055,16 @@ static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
     cfg.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = KS_PDL;
+    at[0].val.programmaticStreamSerializationAllowed = (KS_PDL && pdl) ? 1 : 0;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+template <typename... KArgs, typename... Args>
+static cudaError_t launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                          Args &&...args)
+{
+    return launch_pdl(true, kern, grid, block, smem, stream, std::forward<Args>(args)...);
 }
 
 // Small reset kernel (replaces memset nodes, which would break the PDL chain).
@@ -2047,8 +2092,11 @@ FastLayout fast_layout(long long n, long long nseg0)
     const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
-    L.ch_cap = (int)(n / kChunk + L.seg_cap + 1);
-    L.mat_cap = (psum + L.seg_cap) * 2 + (long long)(kPMax + 1) * (2 * (n / kChunk) + 4);
+    // chunks of one pass: sum over segments of cdiv(len, chunk), chunk >= max(kChunkMin, total / items)
+    const long long nch = std::max(std::min(n / kChunkMin, (long long)kChunkItemsMax), n / kChunk) + 1;
+    L.ch_cap = (int)(nch + L.seg_cap + 1);
+    // sum of (P_s + 1)(nch_s + 1) over segments, P_s + 1 <= min(kPMax + 1, len / kKeysPerPivot + 2)
+    L.mat_cap = (psum + L.seg_cap) * 2 + (long long)(kPMax + 1) * (nch + 4);
     // warp units and fill items of one leaf launch: disjoint final ranges of > kTinyGap keys
     L.unit_cap = (int)(2 * (n / (kTinyGap + 1)) + n / kFillPiece + nseg0 + 4096);
     L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
@@ -2279,7 +2327,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0};
         K.run(kPhPivots, [&] {
             launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
-                   L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next);
+                   L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next,
+                   std::min(g_count, g_scatter));
         });
         if (level == 0 && d_off == nullptr) {   // one segment, known P: build the pivots GPU-wide
             const int P0 = pivots_for(n, kPMax);
@@ -2300,12 +2349,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         }
         if (level == 0)
             K.run(kPhCount, [&] {
-                launch(k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
+                launch_pdl(kPdlHeavy, k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
                        chunk_seg, st, src, piv, lut, mat, st);
             });
         else
             K.run(kPhCount, [&] {
-                launch(k_count<false>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
+                launch_pdl(kPdlHeavy, k_count<false>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
                        chunk_seg, st, src, piv, lut, mat, st);
             });
 #if KS_SCAN3
@@ -2319,7 +2368,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         });
 #endif
         K.run(kPhScatter, [&] {
-            launch(k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur], chunk_seg,
+            launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur], chunk_seg,
                    st, src, dst, piv, lut, moff, mat);
         });
         K.run(kPhPlan, [&] {
@@ -2333,7 +2382,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // CTA shapes (hand-backs go to the next leaf epoch), the warp units and fills
     auto leaf = [&]() {
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1};
-        K.run(kPhLeaf, [&] { launch(k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
+        K.run(kPhLeaf, [&] { launch_pdl(kPdlHeavy, k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // queue claims reset before the small sorts (their hand-backs belong to the next epoch)
         K.run(kPhGate, [&] {   // (bookkeeping launches are booked under "gate")
             launch(k_set_ints, dim3(1), dim3(32), 0, stream,
@@ -2343,11 +2392,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         LeafQ Qn = Q;
         ++Qn.epoch;
         K.run(kPhLeaf, [&] {
-            launch(k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, Q.small[1],
+            launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, Q.small[1],
                    &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
         });
         K.run(kPhLeaf, [&] {
-            launch(k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
+            launch_pdl(kPdlHeavy, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
                    &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
         });
         K.run(kPhGate, [&] {

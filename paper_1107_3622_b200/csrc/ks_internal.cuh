@@ -32,7 +32,14 @@ constexpr int kKeysPerPivot = 2048;   // P = len / 2048 (capped): gaps land in t
 #define KS_LOCAL_KPP 2048
 #endif
 constexpr int kKeysPerPivotLocal = KS_LOCAL_KPP;   // local partitions (children mostly for the small sorts)
-constexpr int kChunk = 16384;         // keys per count-matrix column (one CTA work item)
+// keys per count-matrix column (one count / scatter CTA work item): chosen per
+// pass so that a one-segment pass gives every CTA of the pass grid one chunk;
+// passes over several segments keep chunks <= kChunk (a segment's last chunk
+// is short, so long chunks would unbalance them)
+constexpr int kChunk = 16384;
+constexpr int kChunkMin = 2048;
+constexpr int kChunkAlign = 512;
+constexpr int kChunkItemsMax = 2048;  // bound on the pass grid used for the chunk size
 constexpr int kCountThreads = 512;
 constexpr int kTile = 4096;           // keys staged in shared memory per scatter step
 constexpr int kPassThreads = 512;     // threads of scatter CTAs (8 keys each per tile)
@@ -97,7 +104,7 @@ struct DevStatus {
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
     int scan_next;                    // tile counter of the single-pass count-matrix scan
-    int pad;
+    int chunk;                        // keys per chunk of the current level
     unsigned long long bytes_moved;   // algorithmic bytes, all passes
     unsigned long long phase_bytes[8];  // per phase (ksort.h KS_FLAG_PROFILE numbering)
     unsigned long long keys_partitioned;

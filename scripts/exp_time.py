@@ -15,7 +15,7 @@ pristine = K.generate_device(n, 20260816, kind)
 keys = torch.empty_like(pristine)
 flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 ts = []
-for r in range(13):
+for r in range(int(os.environ.get("EXP_REPS", "13"))):
     keys.copy_(pristine); flush.zero_(); torch.cuda.synchronize()
     a = torch.cuda.Event(enable_timing=True); b = torch.cuda.Event(enable_timing=True)
     a.record(); K.k_sort(keys); b.record(); torch.cuda.synchronize()
