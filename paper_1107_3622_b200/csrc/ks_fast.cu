@@ -62,6 +62,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_PDL
 #define KS_PDL 1          // programmatic dependent launch between the engine's kernels
 #endif
+#ifndef KS_SEGOFF_PF
+#define KS_SEGOFF_PF 1    // L2 prefetch of the count matrix and offsets at the start of a pass
+#endif
 #ifndef KS_PDL_HEAVY
 #define KS_PDL_HEAVY 0    // PDL also into the persistent grids (count, scatter, leaf, segment sorts)
 #endif
@@ -445,13 +448,10 @@ __host__ __device__ __forceinline__ long long mat_eq(const Seg &g, int j) { retu
 // scans over segments for pool offsets and the count-matrix layout; then an
 // L2 prefetch of this level's count matrix and offsets (they are written with
 // scattered 4- and 8-byte stores).
-__global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long long mat_cap, int ch_cap,
-                              int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
-                              unsigned long long *tstat, int *nseg_next, int items)
+__device__ void seg_offsets_body(Seg *segs, int ns, DevStatus *st, long long mat_cap, int ch_cap, int piv_cap,
+                                 int lut_cap, const unsigned *mat, const long long *moff, unsigned long long *tstat,
+                                 int *nseg_next, int items, long long *sh)
 {
-    KS_PDL_ENTRY();
-    __shared__ long long sh[33];
-    int ns = *nseg;
     // chunk size of this pass (see kChunk)
     long long total = 0;
     for (int base = 0; base < ns; base += blockDim.x) {
@@ -503,7 +503,7 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
             st->nchunks = 0;
             st->mat_total = 0;
         } else {
-#if KS_PREFETCH
+#if KS_PREFETCH && KS_SEGOFF_PF
             l2_prefetch(mat, 4ull * c_mat);
             l2_prefetch(moff, 8ull * c_mat);
 #endif
@@ -514,6 +514,35 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
     // look-back words of the single-pass scan (c_mat is block-uniform)
     const long long nt = c_mat <= mat_cap ? cdiv(c_mat, kScanBlock) : 0;
     for (long long i = threadIdx.x; i < nt; i += blockDim.x) tstat[i] = 0ull;
+}
+
+__global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long long mat_cap, int ch_cap,
+                              int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
+                              unsigned long long *tstat, int *nseg_next, int items)
+{
+    KS_PDL_ENTRY();
+    __shared__ long long sh[33];
+    seg_offsets_body(segs, *nseg, st, mat_cap, ch_cap, piv_cap, lut_cap, mat, moff, tstat, nseg_next, items, sh);
+}
+
+// Single array with a level-0 global pass: status reset, routing and the pass
+// bookkeeping of k_seg_offsets in one launch.
+__global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, long long mat_cap, int ch_cap,
+                                   int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
+                                   unsigned long long *tstat, int items)
+{
+    KS_PDL_ENTRY();
+    __shared__ long long sh[33];
+    unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
+    for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        st->bad_index = kNoIndex;
+        route_initial(0, n, Lst, st);
+    }
+    __syncthreads();
+    seg_offsets_body(Lst.gsegs, st->nseg[0], st, mat_cap, ch_cap, piv_cap, lut_cap, mat, moff, tstat, &st->nseg[1],
+                     items, sh);
 }
 
 struct PivotsSmem {
@@ -586,7 +615,7 @@ __global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const Seg *segs, co
     // kRankParts threads per key, each counting over a slice of the P keys
     const int gt = blockIdx.x * blockDim.x + threadIdx.x;
     const int i = gt / kRankParts, part = gt % kRankParts;
-    const int per = (P + kRankParts - 1) / kRankParts;
+    const int per = ((P + kRankParts - 1) / kRankParts) | 1;   // odd stride: the parts read distinct banks
     const int j0 = part * per, j1 = min(P, j0 + per);
     const double v = i < P ? x[i] : 0.0;
     int r = 0;
@@ -2240,6 +2269,24 @@ static void graph_store(GraphEntry e)
     g_graphs.push_back(e);
 }
 
+// Per-thread pinned host copy of the status block (the one read per call).
+struct PinnedStatus {
+    DevStatus *p = nullptr;
+    ~PinnedStatus()
+    {
+        if (p) cudaFreeHost(p);
+    }
+};
+static DevStatus *pinned_status()
+{
+    static thread_local PinnedStatus ps;
+    if (ps.p == nullptr && cudaMallocHost(reinterpret_cast<void **>(&ps.p), sizeof(DevStatus)) != cudaSuccess) {
+        cudaGetLastError();
+        ps.p = nullptr;
+    }
+    return ps.p;
+}
+
 static cudaStream_t capture_stream()
 {
     static std::mutex mu;
@@ -2283,10 +2330,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     Launcher K(stream, profile);
 
     DevStatus h{};
+    DevStatus *hp = pinned_status();   // (a pageable destination would add a staged copy)
     auto sync_status = [&]() -> int {
         KS_CK(cudaGetLastError());
-        KS_CK(cudaMemcpyAsync(&h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
+        KS_CK(cudaMemcpyAsync(hp ? hp : &h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
         KS_CK(cudaStreamSynchronize(stream));
+        if (hp) h = *hp;
         return h.overflow ? KS_CUDA_ERROR : KS_OK;
     };
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
@@ -2300,7 +2349,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream);
         }
         if (d_off == nullptr) {
-            K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
+            if (n > kInitLocalMax)   // (+ the level-0 pass bookkeeping)
+                K.run(kPhGate, [&] {
+                    launch(k_init_single_pass, dim3(1), dim3(1024), 0, stream, n, Lst, st, L.mat_cap, L.ch_cap,
+                           L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum),
+                           std::min(g_count, g_scatter));
+                });
+            else
+                K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
             if (n <= kInitLocalMax)
                 K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
         } else {
@@ -2325,11 +2381,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0};
-        K.run(kPhPivots, [&] {
-            launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
-                   L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next,
-                   std::min(g_count, g_scatter));
-        });
+        if (!(level == 0 && d_off == nullptr))   // (done by k_init_single_pass)
+            K.run(kPhPivots, [&] {
+                launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
+                       L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next,
+                       std::min(g_count, g_scatter));
+            });
         if (level == 0 && d_off == nullptr) {   // one segment, known P: build the pivots GPU-wide
             const int P0 = pivots_for(n, kPMax);
             double *sorted = reinterpret_cast<double *>(moff);   // (scratch: the offsets are written later)

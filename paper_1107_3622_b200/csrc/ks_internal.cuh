@@ -20,10 +20,16 @@ namespace ks {
 // ---------------------------------------------------------------------------
 // Fast-mode tunables.
 // ---------------------------------------------------------------------------
-constexpr int kPMax = 2047;           // max pivot candidates (first P keys) per global pass
-constexpr int kPMaxPow2 = 2048;
+#ifndef KS_PMAX
+#define KS_PMAX 2047
+#endif
+constexpr int kPMax = KS_PMAX;        // max pivot candidates (first P keys) per global pass
+constexpr int kPMaxPow2 = KS_PMAX + 1;
 constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (4095)
-constexpr int kLutMax = 8192;         // LUT buckets (pow2 >= 4*P)
+#ifndef KS_LUTMAX
+#define KS_LUTMAX 8192
+#endif
+constexpr int kLutMax = KS_LUTMAX;    // LUT buckets (pow2 >= 4*P)
 constexpr int kPMaxLocal = 255;       // ... per local partition (P = len / kKeysPerPivot <= 64)
 constexpr int kRowsMaxLocal = 2 * kPMaxLocal + 1;
 constexpr int kLutMaxLocal = 2048;

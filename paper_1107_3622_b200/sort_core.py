@@ -81,13 +81,26 @@ last_stats = SortStats()
 # device plumbing
 # ---------------------------------------------------------------------------
 
+_cuda_ok = False
+
+
 def _device() -> torch.device:
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_1107_3622_b200 needs a CUDA device (B200); there is no CPU fallback")
+    global _cuda_ok
+    if not _cuda_ok:
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_1107_3622_b200 needs a CUDA device (B200); there is no CPU fallback")
+        _cuda_ok = True
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream_ptr() -> int:
+    """The caller's current CUDA stream (the raw handle: ~0.3 us instead of ~3 us
+    for building a torch.cuda.Stream object on every call)."""
+    if _raw_stream is not None:
+        return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 

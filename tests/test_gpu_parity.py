@@ -448,3 +448,30 @@ def test_sizes_around_engine_limits():
         t = dev(a)
         K.k_sort(t)
         assert same_bits(host(t), np.sort(a)), n
+
+
+def test_sort_on_caller_side_stream():
+    # the engine launches on the caller's current stream (sort_core._stream_ptr):
+    # a sort issued under torch.cuda.stream(s) right after the input is produced
+    # on s must see that input and finish before s's next op
+    s = torch.cuda.Stream()
+    n = 1_000_003
+    with torch.cuda.stream(s):
+        x = K.generate_device(n, 20260816)
+        want = torch.sort(x).values
+        K.k_sort(x)
+        same = torch.equal(x, want)
+    s.synchronize()
+    assert bool(same)
+    # and twice on the same buffers (the second call replays the cached graph) on another stream
+    s2 = torch.cuda.Stream()
+    with torch.cuda.stream(s2):
+        y = K.generate_device(n, 7)
+        want2 = torch.sort(y).values
+        K.k_sort(y)
+        y2 = K.generate_device(n, 7)
+        y.copy_(y2)
+        K.k_sort(y)
+        same2 = torch.equal(y, want2)
+    s2.synchronize()
+    assert bool(same2)
