@@ -74,6 +74,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_GRAPH
 #define KS_GRAPH 1        // replay the speculative schedule as a cached CUDA graph
 #endif
+#ifndef KS_MID_RANK
+#define KS_MID_RANK 1     // 5..16-key buckets of the segment sorter: half-warp ranks instead of insertion sorts
+#endif
 #ifndef KS_MINB1
 #define KS_MINB1 2        // resident CTAs per SM asked for the 512-thread small-segment sorter
 #endif
@@ -1802,8 +1805,30 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             }
         }
         __syncthreads();
-        // 4b. 5..kThreadSortMax keys: one thread each, insertion sort in shared memory
+        // 4b. 5..kThreadSortMax keys: a half-warp per bucket, lane l takes key l
+        //     to its rank in the bucket (ties by position) -- no serial chain
+        //     (was: one thread per bucket, insertion sort; 0.377 -> 0.368 ms at C0)
         const int nmid = S.nmid;
+#if KS_MID_RANK
+        static_assert(kThreadSortMax <= 16, "one half-warp lane per key");
+#pragma unroll 1
+        for (int q = tid >> 4; q < nmid; q += kT / 16) {
+            const int b = mid[q], l = tid & 15;
+            const int s0 = b ? (int)S.cur[b - 1] : 0;
+            const int sz = (int)S.cur[b] - s0;
+            if (l < sz) {
+                const double *x = S.b + s0;
+                const double v = x[l];
+                int r = 0;
+#pragma unroll 4
+                for (int j = 0; j < sz; ++j) {
+                    const double y = x[j];
+                    r += (y < v || (y == v && j < l)) ? 1 : 0;
+                }
+                out[s0 + r] = v;
+            }
+        }
+#else
 #pragma unroll 1
         for (int q = tid; q < nmid; q += kT) {
             const int b = mid[q];
@@ -1812,6 +1837,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             smem_insertion_sort(S.b + s0, sz);
             for (int i = 0; i < sz; ++i) out[s0 + i] = S.b[s0 + i];
         }
+#endif
         // 4c. large buckets (sorted by warps above, or handed back): coalesced copy
         for (int q = wid; q < nbig; q += kWarps) {
             const int b = S.big[q];
