@@ -373,6 +373,18 @@ def run_ours(args):
                        "frac_of_8tbs": multi_pass_gbs / 8000.0, "levels": stats.levels,
                        "leaves": stats.leaves, "keys_leaf_sorted": stats.keys_leaf_sorted,
                        "ideal_single_pass_frac": (16 * n / (ms_per_step * 1e-3) / 1e9) / hbm},
+        # the north star's multi-pass roofline: the traffic of K-sort's own partition
+        # passes (~16.5 passes x 16 B = 264 B/key with on-chip
+        # leaves of <= 8192 keys; the full reference tree: 30.4 x 16 B = 486 B/key)
+        # at peak HBM bandwidth, against this step time (frac > 1: faster than
+        # streaming K-sort's passes at peak)
+        "ksort_multi_pass_roofline": {
+            "bytes_per_key": KSORT_PASS_BYTES_PER_KEY, "peak_gbs": hbm,
+            "floor_ms": KSORT_PASS_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3,
+            "frac": (KSORT_PASS_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3) / ms_per_step,
+            "full_tree_bytes_per_key": KSORT_TREE_BYTES_PER_KEY,
+            "full_tree_frac": (KSORT_TREE_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3) / ms_per_step,
+            "source": "SURVEY.md 8(d) and Appendix C (uniform U[0,1) inputs)"},
         "phases": phase,
         "step_ms": step_ms,
         "clocks": clk.summary(),
@@ -382,6 +394,10 @@ def run_ours(args):
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(n, args.kind)
     print(json.dumps(line), flush=True)
+
+
+KSORT_PASS_BYTES_PER_KEY = 16.0 * 16.5    # K-sort partition passes down to 8192-key leaves
+KSORT_TREE_BYTES_PER_KEY = 16.0 * 30.4    # the reference's full recursion tree
 
 
 def main():

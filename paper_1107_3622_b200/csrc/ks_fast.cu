@@ -77,6 +77,12 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_MID_RANK
 #define KS_MID_RANK 1     // 5..16-key buckets of the segment sorter: half-warp ranks instead of insertion sorts
 #endif
+#ifndef KS_FUSED_HIST
+#define KS_FUSED_HIST 1   // bounded leaf items: bucket histogram built while loading (no min / max pass)
+#endif
+#ifndef KS_SEG_FEED
+#define KS_SEG_FEED 1     // small-segment sorters: next item claimed / fetched / prefetched without stalls
+#endif
 #ifndef KS_MINB1
 #define KS_MINB1 2        // resident CTAs per SM asked for the 512-thread small-segment sorter
 #endif
@@ -122,6 +128,25 @@ __device__ __forceinline__ Seg make_seg(long long start, long long len, int src)
     g.start = start;
     g.len = len;
     g.src = src;
+    return g;
+}
+
+// leaf item with the value range of its keys (blo <= key <= bhi; +-inf: unknown)
+__device__ __forceinline__ Seg make_bseg(long long start, long long len, int src, double blo, double bhi)
+{
+    Seg g = make_seg(start, len, src);
+    g.bnd = (isfinite(blo) && isfinite(bhi)) ? 1 : 0;
+    g.lo = blo;
+    g.scale = bhi;
+    return g;
+}
+// a queued leaf item as published (bounds included)
+__device__ __forceinline__ Seg load_item(const Seg *q)
+{
+    Seg g = make_seg(__ldcg(&q->start), __ldcg(&q->len), __ldcg(&q->src));
+    g.bnd = __ldcg(&q->bnd);
+    g.lo = __ldcg(&q->lo);
+    g.scale = __ldcg(&q->scale);
     return g;
 }
 
@@ -1179,17 +1204,108 @@ __device__ __forceinline__ void tiny_sort_copy(const double *src, double *dst, i
 //  * kSortMax < gap <= kLocalMax            -> local queue
 //  * gap > kLocalMax                        -> next global pass
 //  * equality run <= kFillDirect            -> written right here; longer -> fill item
+//
+// Merging: consecutive pairs of <= kMergeCand keys (gap + a short equality
+// run) are grouped, within runs of such pairs, by floor(run prefix / kMergeT),
+// and a group of two or more pairs is sorted as ONE small segment (its pivots'
+// runs included: they are written into the data buffer too), so the segment
+// sorter sees fewer, larger segments.  Groups hold < kMergeT + kMergeCand keys.
+// `mg` is block-sized shared scratch.
+#ifndef KS_MERGE
+#define KS_MERGE 1
+#endif
+#ifndef KS_MERGE_CAND
+#define KS_MERGE_CAND 4096
+#endif
+#ifndef KS_MERGE_T
+#define KS_MERGE_T 2048
+#endif
+constexpr int kMergeCand = KS_MERGE_CAND, kMergeT = KS_MERGE_T;
+static_assert(kMergeCand + kMergeT <= sort_cap(1) && kMergeCand <= sort_cap(1), "merged groups are small segments");
+__device__ __forceinline__ bool mg_prev_cand(int *mg, bool cand)
+{
+    mg[threadIdx.x] = cand ? 1 : 0;
+    __syncthreads();
+    const bool p = threadIdx.x > 0 && mg[threadIdx.x - 1] != 0;
+    __syncthreads();
+    return p;
+}
+__device__ __forceinline__ long long block_inclusive_max(long long x, long long *sh)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    long long inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const long long y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = y > inc ? y : inc;
+    }
+    if (lane == 31) sh[wid] = inc;
+    __syncthreads();
+    long long w = -1;
+    for (int q = 0; q < wid && q < nw; ++q) w = sh[q] > w ? sh[q] : w;
+    __syncthreads();
+    return w > inc ? w : inc;
+}
+
+__device__ __forceinline__ double block_inclusive_max_f64(double x, long long *sh)
+{
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    double inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = y > inc ? y : inc;
+    }
+    double *shd = reinterpret_cast<double *>(sh);
+    if (lane == 31) shd[wid] = inc;
+    __syncthreads();
+    double w = -CUDART_INF;
+    for (int q = 0; q < wid && q < nw; ++q) w = shd[q] > w ? shd[q] : w;
+    __syncthreads();
+    return w > inc ? w : inc;
+}
+
 __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
-                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase)
+                              const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase, int *mg, double blo,
+                              double bhi)
 {
     int u_gap = 0, s_gap = 0, l_gap = 0, g_gap = 0, t_gap = 0;
-    if (have && (gl >= 2 || (gl == 1 && dst_id == 1))) {
+    bool merged = false;
+#if KS_MERGE
+    if (KS_MERGE == 2 || !A.in_leaf) {   // (block-uniform; in the leaf it costs more than it saves)
+        const long long sz = gl + el;
+        const bool cand = have && sz <= kMergeCand && el <= kFillDirect;
+        const long long x = block_exclusive_scan(cand ? sz : 0, sh, nullptr);   // (non-candidates add 0)
+        const bool prev_cand = mg_prev_cand(mg, cand);
+        // prefix at the start of this pair's run: X is non-decreasing, so the
+        // latest run start carries the largest X
+        const long long xr = block_inclusive_max(cand && !prev_cand ? x : -1, sh);
+        const int key = cand ? (int)((x - xr) / kMergeT) : -1;
+        mg[threadIdx.x] = key;
+        __syncthreads();
+        const bool leader = cand && (threadIdx.x == 0 || mg[threadIdx.x - 1] != key);
+        const bool last = cand && (threadIdx.x + 1 == (int)blockDim.x || mg[threadIdx.x + 1] != key);
+        const long long agl = block_inclusive_max(leader ? ag : -1, sh);   // gaps are in order: latest leader
+        const double glo = block_inclusive_max_f64(leader ? blo : -CUDART_INF, sh);   // ... and so are their bounds
+        merged = cand && !(leader && last);
+        if (merged) {
+            if (dst_id && el > 0)   // the run is part of the merged segment's data
+                for (long long i = 0; i < el; ++i) const_cast<double *>(A.tmp)[ae + i] = pv;
+            if (last) {
+                const long long len = ag + gl + el - agl;
+                small_push(A.Q, make_bseg(agl, len, dst_id, glo, bhi), st);
+            }
+        }
+        __syncthreads();   // mg reuse
+    }
+#endif
+    if (have && !merged && (gl >= 2 || (gl == 1 && dst_id == 1))) {
         if (gl <= kTinyGap) {
             tiny_sort_copy((dst_id ? A.tmp : A.keys) + ag, A.keys + ag, (int)gl);
             t_gap = 1;
         }
         else if (gl <= kUnitMax) u_gap = 1;
-        else if (gl <= sort_cap(1)) small_push(A.Q, make_seg(ag, gl, dst_id), st);
+        else if (gl <= sort_cap(1)) small_push(A.Q, make_bseg(ag, gl, dst_id, blo, bhi), st);
         else if (gl <= kSortMax) s_gap = 1;
         else if (gl <= kLocalMax) l_gap = 1;
         else g_gap = 1;
@@ -1231,16 +1347,16 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     }
     if (s_gap)
         q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, (int)(sbase[3] + pk_get(xpk, kPkS, 11)),
-                  with_kind(make_seg(ag, gl, dst_id), kItemSort), A.Q.epoch);
+                  with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemSort), A.Q.epoch);
     if (l_gap) {
         const int i = (int)(sbase[1] + pk_get(xpk, kPkL, 11));
-        const Seg c = with_kind(make_seg(ag, gl, dst_id), kItemLocal);
+        const Seg c = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal);
         if (A.in_leaf) q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, i, c, A.Q.epoch);
         else if (i < A.Q.lcap) A.Q.lq[A.Q.lcap - 1 - i] = c; else st->overflow = 7;   // (read after this launch)
     }
     if (lb_gap) {
         const int i = (int)(sbase[4] + pk_get(xpk, kPkLB, 11));
-        if (i < A.Q.lcap) A.Q.lq[i] = with_kind(make_seg(ag, gl, dst_id), kItemLocal); else st->overflow = 7;
+        if (i < A.Q.lcap) A.Q.lq[i] = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal); else st->overflow = 7;
     }
     if (g_gap) {
         const long long gi = sbase[2] + pk_get(xpk, kPkG, 11);
@@ -1285,6 +1401,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
     KS_PDL_ENTRY();
     __shared__ long long sh[33];
     __shared__ long long sbase[5];
+    __shared__ int s_mg[kPlanThreads];
     if (abort_requested(st)) return;
     const int ns = *nseg;
     const int j0 = blockIdx.y * kPlanThreads;
@@ -1306,7 +1423,11 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
                 pv = piv_pool[g.piv_off + j];
             }
         }
-        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase);
+        // value range of gap j: (piv[j-1], piv[j]); the ends of the segment: unknown
+        const double blo = (have && j > 0) ? piv_pool[g.piv_off + j - 1] : -CUDART_INF;
+        const double bhi = (have && j < g.k) ? pv : CUDART_INF;
+        const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase, s_mg, blo,
+                                     bhi);
         if (threadIdx.x == 0) {
             // keys of this chunk's classes [2 j0, 2 min(j0 + kPlanThreads, k + 1))
             const int jend = min(j0 + kPlanThreads, g.k + 1);
@@ -1331,6 +1452,7 @@ struct LocalSmem {
     unsigned cursor[kRowsMaxLocal + 1];
     long long sh[33];
     long long sbase[5];
+    int mg[kLocalThreads];
 };
 
 // Partition one local segment (in global memory, L2-resident) with its first
@@ -1408,7 +1530,11 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
             pv = L.piv[j];
         }
     }
-    const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase);
+    // value range of gap j: (piv[j-1], piv[j]), the segment's own bounds at its ends
+    const double blo = (have && j > 0) ? L.piv[j - 1] : (g.bnd ? g.lo : -CUDART_INF);
+    const double bhi = (have && j < k) ? pv : (g.bnd ? g.scale : CUDART_INF);
+    const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase, L.mg, blo,
+                                 bhi);
     if (threadIdx.x == 0) account_partition(st, g.len, o, true);
     KS_TR(3);
 #ifdef KS_TRACE
@@ -1597,9 +1723,54 @@ __device__ __noinline__ bool warp_sort_bucket(double *a, int sz)
 
 // Sort one segment (kUnitMax < len <= kSortMax) on chip and write it to its
 // final place in the user buffer (see the segment-sorter notes above).
-template <int C>
+// Item pipeline of the small-segment sorters, run by thread 0 at two points
+// of each segment so that it never waits: the next item's claim (an atomic
+// issued before the segment) is used after the load phase to start an
+// asynchronous copy of its descriptor into shared memory, and after the
+// scatter phase the copy is complete and its key ranges are prefetched into L2.
+struct NoFeed {
+    __device__ __forceinline__ void after_load() {}
+    __device__ __forceinline__ void after_scatter() {}
+};
+struct SegFeed {
+    const Seg *list;
+    int n;
+    int d;           // claimed next item (thread 0)
+    Seg *slot;       // its descriptor in shared memory
+    int *sidx;
+    const double *keys, *tmp;
+    bool done;
+    __device__ __forceinline__ void after_load()
+    {
+        if (threadIdx.x != 0) return;
+        *sidx = d;
+        if (d < n) {
+            static_assert(sizeof(Seg) % 16 == 0, "descriptor copied in 16-byte pieces");
+            const char *src = reinterpret_cast<const char *>(list + d);
+            const unsigned dst = (unsigned)__cvta_generic_to_shared(slot);
+#pragma unroll
+            for (int o = 0; o < (int)sizeof(Seg); o += 16)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + o), "l"(src + o) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    }
+    __device__ __forceinline__ void after_scatter()
+    {
+        if (done) return;
+        done = true;
+        if (threadIdx.x != 0 || d >= n) return;
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#if KS_PREFETCH
+        const Seg &g = *slot;
+        l2_prefetch((g.src ? tmp : keys) + g.start, 8ull * g.len);
+        if (g.src) l2_prefetch(keys + g.start, 8ull * g.len);
+#endif
+    }
+};
+
+template <int C, typename Feed = NoFeed>
 __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevStatus *st, double *keys,
-                            const double *tmp)
+                            const double *tmp, Feed &&feed = NoFeed{})
 {
 #ifdef KS_TRACE
     long long tr_t0 = clock64();
@@ -1623,10 +1794,45 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     const int m = (int)g.len;
     const double *in = (g.src ? tmp : keys) + start;
     double *out = keys + start;
-    // 1. load (coalesced, 4 loads in flight per thread, L2 only) + min / max
-    double mn = CUDART_INF, mx = -CUDART_INF;
     constexpr int kLU = kT >= 1024 ? 4 : 8;   // loads in flight per thread (one round trip for most segments)
-    for (int i0 = 0; i0 < m; i0 += kLU * kT) {
+    int B = m / Smem::kLam;
+    B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
+    // Bounded item (its keys lie between two of the parent's pivots): the
+    // bucket map is known before the load, so the histogram is built while
+    // loading (no min / max pass, one barrier fewer).  Else: load + min / max.
+    double fscale = 0.0;
+    const bool fused = KS_FUSED_HIST && g.bnd && g.scale > g.lo &&
+                       !((g.lo > 0.0 && g.scale > 64.0 * g.lo) || (g.scale < 0.0 && g.lo < 64.0 * g.scale)) &&
+                       isfinite(fscale = (double)B / (g.scale - g.lo)) && fscale > 0.0;
+    if (fused) {
+#pragma unroll 1
+        for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
+        if (tid == 0) {
+            S.nbig = 0;
+            S.nhb = 0;
+        }
+        __syncthreads();
+        const BucketMap fmap{g.lo, fscale, 0ull, 0, B};
+        for (int i0 = 0; i0 < m; i0 += kLU * kT) {
+            double x[kLU];
+#pragma unroll
+            for (int u = 0; u < kLU; ++u) {
+                const int i = i0 + u * kT + tid;
+                x[u] = i < m ? __ldcg(in + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kLU; ++u) {
+                const int i = i0 + u * kT + tid;
+                if (i < m) {
+                    S.a[i] = x[u];
+                    atomicAdd(&S.cur[fmap(x[u])], 1u);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    double mn = CUDART_INF, mx = -CUDART_INF;
+    for (int i0 = 0; !fused && i0 < m; i0 += kLU * kT) {
         double x[kLU];
 #pragma unroll
         for (int u = 0; u < kLU; ++u) {
@@ -1649,12 +1855,11 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         mn = p < mn ? p : mn;
         mx = q > mx ? q : mx;
     }
+    if (!fused) {
     if (lane == 0) {
         S.red[0][wid] = mn;
         S.red[1][wid] = mx;
     }
-    int B = m / Smem::kLam;
-    B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
 #pragma unroll 1
     for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
     if (tid == 0) {
@@ -1686,21 +1891,27 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
     }
     __syncthreads();
-    const double lo = S.bounds[0];
-    const double scale = S.bounds[1];
+    }
+    const double lo = fused ? g.lo : S.bounds[0];
+    const double scale = fused ? fscale : S.bounds[1];
+    const int bits = fused ? 0 : S.bits;
     KS_TRS(0);   // load + min/max
+    feed.after_load();
     if (scale < 0.0) {   // constant segment: already sorted
         if (g.src) {
 #pragma unroll 1
             for (int i = tid; i < m; i += kT) out[i] = S.a[i];
         }
+        feed.after_scatter();
     } else {
         if (scale == 0.0) B = 1;   // one bucket: the warp path (or the partitioner) takes it
-        const BucketMap bmap{lo, scale, ord_bits(lo), S.bits, B};
-        // 2. bucket histogram, scan, scatter a -> b
+        const BucketMap bmap{lo, scale, ord_bits(lo), bits, B};
+        // 2. bucket histogram (unless built while loading), scan, scatter a -> b
+        if (!fused) {
 #pragma unroll 1
-        for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[bmap(S.a[i])], 1u);
-        __syncthreads();
+            for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[bmap(S.a[i])], 1u);
+            __syncthreads();
+        }
         KS_TRS(1);   // histogram
         {
             const int b0 = tid * Smem::kPB;
@@ -1732,6 +1943,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x;
         }
         __syncthreads();
+        feed.after_scatter();
         KS_TRS(2);   // scan + scatter
         // 3. cur[b] is now the end of bucket b.  Buckets of more than
         //    kThreadSortMax keys (listed by the scan; none for smooth
@@ -1889,6 +2101,31 @@ __global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_M
         }
 #endif
     };
+#if KS_SEG_FEED
+    // descriptors of the current and the next item in shared memory (see SegFeed)
+    __shared__ __align__(16) Seg s_seg[2];
+    __shared__ int s_idx[2];
+    (void)s_item;
+    if (threadIdx.x == 0) {
+        const int d = atomicAdd(next, 1);
+        s_idx[0] = d;
+        if (d < n) {
+            s_seg[0] = list[d];
+            prefetch(d);
+        }
+    }
+    for (int slot = 0;; slot ^= 1) {
+        __syncthreads();
+        if (s_idx[slot] >= n) break;
+        const Seg g = s_seg[slot];
+        SegFeed f{list, n, 0, &s_seg[slot ^ 1], &s_idx[slot ^ 1], keys, tmp, false};
+        if (threadIdx.x == 0) f.d = atomicAdd(next, 1);   // (used after the load phase)
+        segsort_one<C>(S, g, Q, st, keys, tmp, f);
+        f.after_scatter();   // (no-op unless the segment took no scatter path)
+        keys_sorted += (unsigned long long)g.len;
+        segs_sorted += 1;
+    }
+#else
     if (threadIdx.x == 0) {
         s_item = atomicAdd(next, 1);
         prefetch(s_item);
@@ -1908,6 +2145,7 @@ __global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_M
         segs_sorted += 1;
         __syncthreads();
     }
+#endif
     if (threadIdx.x == 0 && segs_sorted) {
         add_bytes(st, kPhLeaf, 16ull * keys_sorted);
         atomicAdd(&st->keys_leaf, keys_sorted);
@@ -1967,7 +2205,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
                 if (idx < lq_n) {
                     const int slot = idx < lq_nb ? idx : Q.lcap - 1 - (idx - lq_nb);
                     const Seg *q = Q.lq + slot;
-                    ctl.seg = make_seg(__ldcg(&q->start), __ldcg(&q->len), __ldcg(&q->src));
+                    ctl.seg = load_item(q);
                     kind = kItemLocal;
                 } else {
                     local_phase = false;
@@ -1981,7 +2219,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
                         const int slot = idx % Q.scap;
                         while (ld_acquire_u64(&Q.sq_ready[slot]) != q_tag(Q.epoch, idx)) __nanosleep(32);
                         const Seg *q = Q.sq + slot;
-                        ctl.seg = make_seg(__ldcg(&q->start), __ldcg(&q->len), __ldcg(&q->src));
+                        ctl.seg = load_item(q);
                         kind = __ldcg(&q->k);
                         break;
                     }

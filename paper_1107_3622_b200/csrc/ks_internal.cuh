@@ -134,7 +134,7 @@ struct Seg {
     int lut_off;       // offset into the LUT pool (T int2 slots)
     int T;             // LUT buckets (1 = plain binary search)
     int src;           // local rounds: 0 keys / 1 tmp hold the segment
-    int pad1;
+    int bnd;           // leaf items: all keys lie in [lo, scale] (bounds from the parent's pivots)
     double lo, scale;  // LUT transform t = clamp((v - lo) * scale, 0, T-1)
 };
 

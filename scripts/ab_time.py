@@ -56,4 +56,5 @@ for r in range(reps + 3):
 for nm, *_ in libs:
     t = sorted(times[nm])
     print(json.dumps({"lib": nm, "n": n, "kind": kind, "ms_median": round(statistics.median(t), 4),
-                      "ms_p20": round(t[len(t) // 5], 4), "ok": ok[nm]}))
+                      "ms_p20": round(t[len(t) // 5], 4), "ms_min": round(t[0], 4), "ms_p80": round(t[(4 * len(t)) // 5], 4),
+                      "ok": ok[nm]}))

@@ -15,8 +15,10 @@ p.add_argument("--reps", type=int, default=2)
 a = p.parse_args()
 pristine = K.generate_device(a.n, 20260816, a.kind)
 keys = torch.empty_like(pristine)
+flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 for _ in range(a.reps):
     keys.copy_(pristine)
+    flush.zero_()   # L2 flushed before each sort, as in bench.py (ncu: run with --cache-control none)
     K.k_sort(keys)
 torch.cuda.synchronize()
 ok = K.is_sorted(keys)

@@ -26,3 +26,16 @@ for rep in range(2):
         segs = max(buf[b + 4], 1)
         print("rep %d class %d: %d segs; cycles/seg load %.0f hist %.0f scan+scatter %.0f order+write %.0f" %
               (rep, c, buf[b + 4], buf[b] / segs, buf[b + 1] / segs, buf[b + 2] / segs, buf[b + 3] / segs))
+buf2 = (ctypes.c_ulonglong * 64)()
+k.copy_(p)
+torch.cuda.synchronize()
+L.ks_trace_read(ctypes.addressof(buf2), 64, 1)
+K.k_sort(k)
+torch.cuda.synchronize()
+L.ks_trace_read(ctypes.addressof(buf2), 64, 0)
+for c in range(3):
+    b = 32 + 8 * c
+    segs = max(buf2[16 + 5 * c + 4], 1)
+    print("class %d: %d segs, %.0f keys/seg; order+write split: pre %.0f | 4a %.0f | sync %.0f | 4b %.0f | 4c %.0f | sync %.0f" %
+          (c, segs, buf2[b + 7] / segs, buf2[b] / segs, buf2[b + 1] / segs, buf2[b + 2] / segs, buf2[b + 3] / segs,
+           buf2[b + 4] / segs, buf2[b + 5] / segs))
