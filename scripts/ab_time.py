@@ -17,6 +17,7 @@ import paper_1107_3622_b200 as K  # noqa: E402
 n = int(os.environ.get("EXP_N", "10000000"))
 kind = os.environ.get("EXP_KIND", "uniform01")
 reps = int(os.environ.get("EXP_REPS", "40"))
+batch = int(os.environ.get("EXP_BATCH", "0"))   # C4 shape: EXP_BATCH arrays of EXP_N keys, one segmented call
 libs = []
 for path in sys.argv[1:]:
     L = ctypes.CDLL(os.path.abspath(path))
@@ -25,11 +26,19 @@ for path in sys.argv[1:]:
     L.ks_sort_f64.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p,
                               ctypes.c_uint32, ctypes.POINTER(_lib.KsStatus)]
     L.ks_sort_f64.restype = ctypes.c_int
-    wsb = L.ks_workspace_bytes(n, 1, 0)
+    L.ks_sort_f64_segmented.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                                        ctypes.c_size_t, ctypes.c_void_p, ctypes.c_uint32, ctypes.POINTER(_lib.KsStatus)]
+    L.ks_sort_f64_segmented.restype = ctypes.c_int
+    wsb = L.ks_workspace_bytes(n * max(1, batch), max(1, batch), 0)
     libs.append((os.path.basename(path), L, torch.empty(wsb, dtype=torch.uint8, device="cuda"), wsb))
 
-pristine = K.generate_device(n, 20260816, kind)
-want = torch.sort(pristine).values
+if batch:
+    pristine = torch.cat([K.generate_device(n, 20260816 + r, kind) for r in range(batch)])
+    off = torch.arange(batch + 1, dtype=torch.int64, device="cuda") * n
+    want = torch.sort(pristine.view(batch, n), dim=1).values.reshape(-1)
+else:
+    pristine = K.generate_device(n, 20260816, kind)
+    want = torch.sort(pristine).values
 keys = torch.empty_like(pristine)
 flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 stream = torch.cuda.current_stream()
@@ -44,7 +53,11 @@ for r in range(reps + 3):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        rc = L.ks_sort_f64(keys.data_ptr(), n, ws.data_ptr(), wsb, stream.cuda_stream, 0, ctypes.byref(st))
+        if batch:
+            rc = L.ks_sort_f64_segmented(keys.data_ptr(), off.data_ptr(), batch, n * batch, ws.data_ptr(), wsb,
+                                         stream.cuda_stream, 0, ctypes.byref(st))
+        else:
+            rc = L.ks_sort_f64(keys.data_ptr(), n, ws.data_ptr(), wsb, stream.cuda_stream, 0, ctypes.byref(st))
         b.record(stream)
         torch.cuda.synchronize()
         if rc != 0:
