@@ -83,6 +83,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_SEG_FEED
 #define KS_SEG_FEED 1     // small-segment sorters: next item claimed / fetched / prefetched without stalls
 #endif
+#ifndef KS_MINB0
+#define KS_MINB0 5        // resident CTAs per SM asked for the class-0 small-segment sorter
+#endif
 #ifndef KS_MINB1
 #define KS_MINB1 2        // resident CTAs per SM asked for the 512-thread small-segment sorter
 #endif
@@ -1215,10 +1218,10 @@ __device__ __forceinline__ void tiny_sort_copy(const double *src, double *dst, i
 #define KS_MERGE 1
 #endif
 #ifndef KS_MERGE_CAND
-#define KS_MERGE_CAND 4096
+#define KS_MERGE_CAND (2 * sort_cap(1) / 3)
 #endif
 #ifndef KS_MERGE_T
-#define KS_MERGE_T 2048
+#define KS_MERGE_T (sort_cap(1) / 3)
 #endif
 constexpr int kMergeCand = KS_MERGE_CAND, kMergeT = KS_MERGE_T;
 static_assert(kMergeCand + kMergeT <= sort_cap(1) && kMergeCand <= sort_cap(1), "merged groups are small segments");
@@ -2078,7 +2081,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 // shape pull them from a counter after the leaf launch.  Hand-backs go to the
 // next leaf launch's queue.
 template <int C>
-__global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_MINB1 : 5)
+__global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : KS_MINB1)
     k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp,
               const Item *units)
 {
@@ -2153,7 +2156,7 @@ __global__ void __launch_bounds__(sort_threads(C), sort_threads(C) >= 512 ? KS_M
     }
     if (C == 0) {   // the last kernel of the launch also finishes the warp units and fills
         constexpr int kW = sort_threads(C) / 32;
-        static_assert(kW * sidx_size(kUnitMax) <= 2 * SortSmem<C>::kCap, "unit scratch fits the a + b buffers");
+        static_assert(C != 0 || kW * sidx_size(kUnitMax) <= 2 * SortSmem<C>::kCap, "unit scratch fits the a + b buffers");
         __syncthreads();
         double *sm = S.a + (threadIdx.x >> 5) * sidx_size(kUnitMax);   // (a and b are contiguous)
         const int nu = st->nunits;

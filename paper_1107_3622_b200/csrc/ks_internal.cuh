@@ -76,7 +76,10 @@ constexpr int kSortMax = 12288;
 #ifndef KS_CAP1
 #define KS_CAP1 6144
 #endif
-__host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? 2048 : (c == 1 ? KS_CAP1 : kSortMax); }
+#ifndef KS_CAP0
+#define KS_CAP0 2048
+#endif
+__host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? KS_CAP0 : (c == 1 ? KS_CAP1 : kSortMax); }
 #ifndef KS_T1
 #define KS_T1 512
 #endif

@@ -5,7 +5,7 @@ LIBS=("$@")
 for cfg in "10000000 uniform01" "7000000 uniform01" "1000000 uniform01" "10000000 dup256"; do
   set -- $cfg; n=$1; k=$2; shift 2
   echo "== n=$n kind=$k"
-  EXP_N=$n EXP_KIND=$k EXP_REPS=${EXP_REPS:-30} timeout 300 python scripts/ab_time.py "${LIBS[@]}" 2>&1 | tail -4
+  EXP_N=$n EXP_KIND=$k EXP_REPS=${EXP_REPS:-30} timeout 300 python scripts/ab_time.py "${LIBS[@]}" 2>&1 | grep "^{"
 done
 echo "== C4 500 x 100000"
-EXP_N=100000 EXP_BATCH=500 EXP_REPS=${EXP_REPS:-15} timeout 300 python scripts/ab_time.py "${LIBS[@]}" 2>&1 | tail -4
+EXP_N=100000 EXP_BATCH=500 EXP_REPS=${EXP_REPS:-15} timeout 300 python scripts/ab_time.py "${LIBS[@]}" 2>&1 | grep "^{"
