@@ -83,6 +83,12 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_SEG_FEED
 #define KS_SEG_FEED 1     // small-segment sorters: next item claimed / fetched / prefetched without stalls
 #endif
+#ifndef KS_SINGLE_MIN_N
+#define KS_SINGLE_MIN_N 8000000   // class-1 lists of inputs this large go to the single-buffer sorter (class 3)
+#endif
+#ifndef KS_MINB3
+#define KS_MINB3 3
+#endif
 #ifndef KS_MINB0
 #define KS_MINB0 5        // resident CTAs per SM asked for the class-0 small-segment sorter
 #endif
@@ -1630,13 +1636,17 @@ __device__ void finish_item(const Item &it, double *keys, const double *tmp, dou
 //      depend on the value distribution
 //   4. coalesced write-back.
 // ---------------------------------------------------------------------------
+constexpr int kMidCap = 256;   // listed 5..kThreadSortMax-key buckets (single buffer); beyond: the owner sorts
 template <int C>
 struct SortSmem {
     static constexpr int kT = sort_threads(C), kCap = sort_cap(C), kLam = sort_lambda(C);
+    // single buffer: the keys are read from global memory (L2) once per pass
+    // instead of being held in `a` -- half the shared memory, more sorters per SM
+    static constexpr bool kSingle = C == 3;
     static constexpr int kBuckets = kCap / kLam;            // interpolation buckets
     static constexpr int kPB = kBuckets / kT;               // buckets per thread in the scan
     static constexpr int kBigCap = kCap / (kThreadSortMax + 1) + 1;
-    double a[kCap];        // the segment as loaded
+    double a[kSingle ? 1 : kCap];   // the segment as loaded
     double b[kCap];        // bucket order
     unsigned cur[kBuckets];
     int big[kBigCap];
@@ -1648,7 +1658,27 @@ struct SortSmem {
     int nmid;              // buckets of 5..kThreadSortMax keys (listed in the free `a` buffer)
     int nhb;               // hand-back buckets (published once the segment is written)
     int hb[kCap / (kUnitMax + 1) + 1];
+    int mid[kSingle ? kMidCap : 1];   // (single buffer: no free `a` for the list)
 };
+
+// f(i, key) for every key of in[0, m), kLU loads in flight per thread (L2 only)
+template <int kT, int kLU, typename F>
+__device__ __forceinline__ void for_keys(const double *in, int m, F &&f)
+{
+    for (int i0 = 0; i0 < m; i0 += kLU * kT) {
+        double x[kLU];
+#pragma unroll
+        for (int u = 0; u < kLU; ++u) {
+            const int i = i0 + u * kT + (int)threadIdx.x;
+            x[u] = i < m ? __ldcg(in + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kLU; ++u) {
+            const int i = i0 + u * kT + (int)threadIdx.x;
+            if (i < m) f(i, x[u]);
+        }
+    }
+}
 
 __device__ __forceinline__ int sort_bucket(double v, double lo, double scale, int B)
 {
@@ -1781,7 +1811,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     do {                                                                                \
         if (threadIdx.x == 0) {                                                         \
             long long t1_ = clock64();                                                  \
-            atomicAdd(&g_trace[16 + 5 * C + (slot)], (unsigned long long)(t1_ - tr_t0)); \
+            atomicAdd(&g_trace[16 + 5 * (C == 3 ? 1 : C) + (slot)], (unsigned long long)(t1_ - tr_t0)); \
             tr_t0 = t1_;                                                                \
         }                                                                               \
     } while (0)
@@ -1827,7 +1857,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             for (int u = 0; u < kLU; ++u) {
                 const int i = i0 + u * kT + tid;
                 if (i < m) {
-                    S.a[i] = x[u];
+                    if (!Smem::kSingle) S.a[i] = x[u];
                     atomicAdd(&S.cur[fmap(x[u])], 1u);
                 }
             }
@@ -1846,7 +1876,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         for (int u = 0; u < kLU; ++u) {
             const int i = i0 + u * kT + tid;
             if (i < m) {
-                S.a[i] = x[u];
+                if (!Smem::kSingle) S.a[i] = x[u];
                 mn = x[u] < mn ? x[u] : mn;
                 mx = x[u] > mx ? x[u] : mx;
             }
@@ -1903,7 +1933,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     if (scale < 0.0) {   // constant segment: already sorted
         if (g.src) {
 #pragma unroll 1
-            for (int i = tid; i < m; i += kT) out[i] = S.a[i];
+            for (int i = tid; i < m; i += kT) out[i] = Smem::kSingle ? __ldcg(in + i) : S.a[i];
         }
         feed.after_scatter();
     } else {
@@ -1912,7 +1942,10 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         // 2. bucket histogram (unless built while loading), scan, scatter a -> b
         if (!fused) {
 #pragma unroll 1
-            for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[bmap(S.a[i])], 1u);
+            if (Smem::kSingle)
+                for_keys<kT, kLU>(in, m, [&](int, double x) { atomicAdd(&S.cur[bmap(x)], 1u); });
+            else
+                for (int i = tid; i < m; i += kT) atomicAdd(&S.cur[bmap(S.a[i])], 1u);
             __syncthreads();
         }
         KS_TRS(1);   // histogram
@@ -1940,10 +1973,14 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             }
         }
         __syncthreads();
+        if (Smem::kSingle) {
+            for_keys<kT, kLU>(in, m, [&](int, double x) { S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x; });
+        } else {
 #pragma unroll 1
-        for (int i = tid; i < m; i += kT) {
-            const double x = S.a[i];
-            S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x;
+            for (int i = tid; i < m; i += kT) {
+                const double x = S.a[i];
+                S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x;
+            }
         }
         __syncthreads();
         feed.after_scatter();
@@ -1988,7 +2025,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         // 4a. one thread per bucket: <= 4 keys -> sorting network in registers,
         //     stored straight to the final place; 5..kThreadSortMax keys ->
         //     listed (the `a` buffer is free now) for 4b
-        int *mid = reinterpret_cast<int *>(S.a);
+        int *mid = Smem::kSingle ? S.mid : reinterpret_cast<int *>(S.a);
         if (tid == 0) S.nmid = 0;
         __syncthreads();
 #pragma unroll 1
@@ -2001,7 +2038,13 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 const int sz = (int)S.cur[b] - s0;
                 if (sz == 0 || sz > kThreadSortMax) continue;
                 if (sz > 4) {
-                    mid[atomicAdd(&S.nmid, 1)] = b;
+                    const int q = atomicAdd(&S.nmid, 1);
+                    if (!Smem::kSingle || q < kMidCap) {
+                        mid[q] = b;
+                    } else {   // list full: the owner sorts it
+                        smem_insertion_sort(S.b + s0, sz);
+                        for (int i = 0; i < sz; ++i) out[s0 + i] = S.b[s0 + i];
+                    }
                     continue;
                 }
                 const double *x = S.b + s0;
@@ -2023,7 +2066,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         // 4b. 5..kThreadSortMax keys: a half-warp per bucket, lane l takes key l
         //     to its rank in the bucket (ties by position) -- no serial chain
         //     (was: one thread per bucket, insertion sort; 0.377 -> 0.368 ms at C0)
-        const int nmid = S.nmid;
+        const int nmid = Smem::kSingle ? min(S.nmid, kMidCap) : S.nmid;
 #if KS_MID_RANK
         static_assert(kThreadSortMax <= 16, "one half-warp lane per key");
 #pragma unroll 1
@@ -2072,7 +2115,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
     }
 #ifdef KS_TRACE
-    if (threadIdx.x == 0) atomicAdd(&g_trace[16 + 5 * C + 4], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&g_trace[16 + 5 * (C == 3 ? 1 : C) + 4], 1ull);
 #endif
 #undef KS_TRS
 }
@@ -2081,7 +2124,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 // shape pull them from a counter after the leaf launch.  Hand-backs go to the
 // next leaf launch's queue.
 template <int C>
-__global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : KS_MINB1)
+__global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ? KS_MINB3 : KS_MINB1))
     k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp,
               const Item *units)
 {
@@ -2421,7 +2464,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 // Per-device launch shapes and kernel attributes, set up once per process
 // (cudaFuncSetAttribute / occupancy queries cost host time on every call).
 struct EngineCfg {
-    int sms, g_count, g_scatter, g_leaf, g_small[2];
+    int sms, g_count, g_scatter, g_leaf, g_small[2], g_small3;
 };
 
 static const EngineCfg *engine_cfg()
@@ -2445,6 +2488,7 @@ static const EngineCfg *engine_cfg()
     smem(k_leaf, kLeafSmem);
     smem(k_segsort<0>, sizeof(SortSmem<0>));
     smem(k_segsort<1>, sizeof(SortSmem<1>));
+    smem(k_segsort<3>, sizeof(SortSmem<3>));
     if (!ok) {
         fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
         return nullptr;
@@ -2460,6 +2504,7 @@ static const EngineCfg *engine_cfg()
     c.g_leaf = grid(k_leaf, kLeafThreads, kLeafSmem);
     c.g_small[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
     c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
+    c.g_small3 = grid(k_segsort<3>, sort_threads(3), sizeof(SortSmem<3>));
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -2715,10 +2760,20 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         });
         LeafQ Qn = Q;
         ++Qn.epoch;
-        K.run(kPhLeaf, [&] {
-            launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream, Q.small[1],
-                   &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
-        });
+        // class-1 list: on large inputs (many segments per CTA slot) the
+        // single-buffer sorter (3 per SM, 256 threads) has the higher throughput;
+        // on smaller ones the 512-thread sorter's shorter per-segment latency wins
+        // (measured: 10M keys -2.4%, 500 x 100K -4.0%; 7M +4.4%, 1M +10%)
+        if (n >= KS_SINGLE_MIN_N)
+            K.run(kPhLeaf, [&] {
+                launch_pdl(kPdlHeavy, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sizeof(SortSmem<3>), stream,
+                           Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
+            });
+        else
+            K.run(kPhLeaf, [&] {
+                launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream,
+                           Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
+            });
         K.run(kPhLeaf, [&] {
             launch_pdl(kPdlHeavy, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
                    &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);

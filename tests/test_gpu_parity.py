@@ -440,6 +440,18 @@ def test_skewed_distributions(kind, n):
     assert same_bits(host(t), np.sort(a)), kind
 
 
+@pytest.mark.parametrize("kind", ["exponential", "clusters", "powers_of_two", "bit_patterns"])
+def test_skewed_large_inputs(kind):
+    """Inputs of >= 8M keys take the single-buffer class-1 sorter (KS_SINGLE_MIN_N):
+    skewed buckets, hand-backs and bounded items through that path."""
+    n = 9_000_001
+    rng = np.random.default_rng(hash((kind, n)) % 2**32)
+    a = _skewed(kind, n, rng)
+    t = dev(a)
+    K.k_sort(t)
+    assert same_bits(host(t), np.sort(a)), kind
+
+
 def test_sizes_around_engine_limits():
     """Sizes at every routing threshold (tiny gap, unit, sort classes, on-chip sort, local partition)."""
     rng = np.random.default_rng(3)
