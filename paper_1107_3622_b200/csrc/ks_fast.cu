@@ -86,6 +86,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_SINGLE_MIN_N
 #define KS_SINGLE_MIN_N 8000000   // class-1 lists of inputs this large go to the single-buffer sorter (class 3)
 #endif
+#ifndef KS_MINB4
+#define KS_MINB4 8        // class 4 = class 0's keys by a single-buffer sorter (large inputs)
+#endif
 #ifndef KS_MINB3
 #define KS_MINB3 3
 #endif
@@ -1642,11 +1645,14 @@ struct SortSmem {
     static constexpr int kT = sort_threads(C), kCap = sort_cap(C), kLam = sort_lambda(C);
     // single buffer: the keys are read from global memory (L2) once per pass
     // instead of being held in `a` -- half the shared memory, more sorters per SM
-    static constexpr bool kSingle = C == 3;
+    static constexpr bool kSingle = C == 3 || C == 4;
+    // class 0 also finishes the warp units in `a` + `b` (kUnitScratch doubles)
+    static constexpr int kUnitScratch = (kT / 32) * sidx_size(kUnitMax);
+    static constexpr int kA = !kSingle ? kCap : (C == 4 && kUnitScratch > kCap ? kUnitScratch - kCap : 1);
     static constexpr int kBuckets = kCap / kLam;            // interpolation buckets
     static constexpr int kPB = kBuckets / kT;               // buckets per thread in the scan
     static constexpr int kBigCap = kCap / (kThreadSortMax + 1) + 1;
-    double a[kSingle ? 1 : kCap];   // the segment as loaded
+    double a[kA];          // the segment as loaded (single buffer: unused, or unit scratch)
     double b[kCap];        // bucket order
     unsigned cur[kBuckets];
     int big[kBigCap];
@@ -1811,7 +1817,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     do {                                                                                \
         if (threadIdx.x == 0) {                                                         \
             long long t1_ = clock64();                                                  \
-            atomicAdd(&g_trace[16 + 5 * (C == 3 ? 1 : C) + (slot)], (unsigned long long)(t1_ - tr_t0)); \
+            atomicAdd(&g_trace[16 + 5 * (C == 3 ? 1 : (C == 4 ? 0 : C)) + (slot)], (unsigned long long)(t1_ - tr_t0)); \
             tr_t0 = t1_;                                                                \
         }                                                                               \
     } while (0)
@@ -2115,7 +2121,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
     }
 #ifdef KS_TRACE
-    if (threadIdx.x == 0) atomicAdd(&g_trace[16 + 5 * (C == 3 ? 1 : C) + 4], 1ull);
+    if (threadIdx.x == 0) atomicAdd(&g_trace[16 + 5 * (C == 3 ? 1 : (C == 4 ? 0 : C)) + 4], 1ull);
 #endif
 #undef KS_TRS
 }
@@ -2124,7 +2130,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 // shape pull them from a counter after the leaf launch.  Hand-backs go to the
 // next leaf launch's queue.
 template <int C>
-__global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ? KS_MINB3 : KS_MINB1))
+__global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ? KS_MINB3 : (C == 4 ? KS_MINB4 : KS_MINB1)))
     k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp,
               const Item *units)
 {
@@ -2197,9 +2203,10 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         atomicAdd(&st->keys_leaf, keys_sorted);
         atomicAdd(&st->leaves, segs_sorted);
     }
-    if (C == 0) {   // the last kernel of the launch also finishes the warp units and fills
+    if (C == 0 || C == 4) {   // the last kernel of the launch also finishes the warp units and fills
         constexpr int kW = sort_threads(C) / 32;
-        static_assert(C != 0 || kW * sidx_size(kUnitMax) <= 2 * SortSmem<C>::kCap, "unit scratch fits the a + b buffers");
+        static_assert((C != 0 && C != 4) || kW * sidx_size(kUnitMax) <= SortSmem<C>::kA + SortSmem<C>::kCap,
+                      "unit scratch fits a + b");
         __syncthreads();
         double *sm = S.a + (threadIdx.x >> 5) * sidx_size(kUnitMax);   // (a and b are contiguous)
         const int nu = st->nunits;
@@ -2464,7 +2471,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 // Per-device launch shapes and kernel attributes, set up once per process
 // (cudaFuncSetAttribute / occupancy queries cost host time on every call).
 struct EngineCfg {
-    int sms, g_count, g_scatter, g_leaf, g_small[2], g_small3;
+    int sms, g_count, g_scatter, g_leaf, g_small[2], g_small3, g_small4;
 };
 
 static const EngineCfg *engine_cfg()
@@ -2489,6 +2496,7 @@ static const EngineCfg *engine_cfg()
     smem(k_segsort<0>, sizeof(SortSmem<0>));
     smem(k_segsort<1>, sizeof(SortSmem<1>));
     smem(k_segsort<3>, sizeof(SortSmem<3>));
+    smem(k_segsort<4>, sizeof(SortSmem<4>));
     if (!ok) {
         fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
         return nullptr;
@@ -2505,6 +2513,7 @@ static const EngineCfg *engine_cfg()
     c.g_small[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
     c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
     c.g_small3 = grid(k_segsort<3>, sort_threads(3), sizeof(SortSmem<3>));
+    c.g_small4 = grid(k_segsort<4>, sort_threads(4), sizeof(SortSmem<4>));
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -2774,10 +2783,16 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                 launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream,
                            Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
             });
-        K.run(kPhLeaf, [&] {
-            launch_pdl(kPdlHeavy, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream, Q.small[0],
-                   &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
-        });
+        if (n >= KS_SINGLE_MIN_N)   // (same trade-off for the class-0 list: 8 single-buffer sorters per SM)
+            K.run(kPhLeaf, [&] {
+                launch_pdl(kPdlHeavy, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)), sizeof(SortSmem<4>), stream,
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
+            });
+        else
+            K.run(kPhLeaf, [&] {
+                launch_pdl(kPdlHeavy, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream,
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
+            });
         K.run(kPhGate, [&] {
             launch(k_set_ints, dim3(1), dim3(32), 0, stream,
                    IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,

@@ -81,16 +81,17 @@ constexpr int kSortMax = 12288;
 #endif
 // Size classes of the on-chip segment sorter: 0 (<= KS_CAP0 keys), 1 (<= KS_CAP1),
 // 2 (<= kSortMax, inside the leaf kernel).  Class 3 is class 1's keys sorted by a
-// single-buffer 256-thread sorter (more sorters per SM; chosen for large inputs).
-__host__ __device__ constexpr int sort_cap(int c) { return c == 0 ? KS_CAP0 : ((c == 1 || c == 3) ? KS_CAP1 : kSortMax); }
+// single-buffer 256-thread sorter, class 4 class 0's keys by a single-buffer
+// sorter (more sorters per SM; both chosen for large inputs).
+__host__ __device__ constexpr int sort_cap(int c) { return (c == 0 || c == 4) ? KS_CAP0 : ((c == 1 || c == 3) ? KS_CAP1 : kSortMax); }
 #ifndef KS_T1
 #define KS_T1 512
 #endif
 #ifndef KS_T3
 #define KS_T3 256
 #endif
-__host__ __device__ constexpr int sort_threads(int c) { return c == 0 ? KS_T0 : (c == 1 ? KS_T1 : (c == 3 ? KS_T3 : 1024)); }
-__host__ __device__ constexpr int sort_lambda(int c) { return c == 0 ? KS_LAM0 : ((c == 1 || c == 3) ? KS_LAM1 : 2); }   // keys per bucket
+__host__ __device__ constexpr int sort_threads(int c) { return (c == 0 || c == 4) ? KS_T0 : (c == 1 ? KS_T1 : (c == 3 ? KS_T3 : 1024)); }
+__host__ __device__ constexpr int sort_lambda(int c) { return (c == 0 || c == 4) ? KS_LAM0 : ((c == 1 || c == 3) ? KS_LAM1 : 2); }   // keys per bucket
 __host__ __device__ __forceinline__ int sort_class(long long len) { return len <= sort_cap(0) ? 0 : (len <= sort_cap(1) ? 1 : 2); }
 constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
 #ifndef KS_LOCAL_THREADS
