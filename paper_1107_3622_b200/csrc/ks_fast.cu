@@ -92,6 +92,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_MINB3
 #define KS_MINB3 3
 #endif
+#ifndef KS_SINGLE2
+#define KS_SINGLE2 0      // the leaf's class-2 sorter with a single shared buffer (room for larger segments)
+#endif
 #ifndef KS_MINB0
 #define KS_MINB0 5        // resident CTAs per SM asked for the class-0 small-segment sorter
 #endif
@@ -1645,7 +1648,7 @@ struct SortSmem {
     static constexpr int kT = sort_threads(C), kCap = sort_cap(C), kLam = sort_lambda(C);
     // single buffer: the keys are read from global memory (L2) once per pass
     // instead of being held in `a` -- half the shared memory, more sorters per SM
-    static constexpr bool kSingle = C == 3 || C == 4;
+    static constexpr bool kSingle = C == 3 || C == 4 || (C == 2 && KS_SINGLE2);
     // class 0 also finishes the warp units in `a` + `b` (kUnitScratch doubles)
     static constexpr int kUnitScratch = (kT / 32) * sidx_size(kUnitMax);
     static constexpr int kA = !kSingle ? kCap : (C == 4 && kUnitScratch > kCap ? kUnitScratch - kCap : 1);

@@ -63,7 +63,10 @@ constexpr int kTinyGap = 16;          // gaps up to this are sorted by the emitt
 // classes, each with its own CTA shape so that every thread holds 12..16 keys:
 //   class 0: <= 2048 keys, 128 threads;  class 1: <= 6144, 512;  class 2: <= 12288, 1024
 constexpr int kSortClasses = 3;
-constexpr int kSortMax = 12288;
+#ifndef KS_SORTMAX
+#define KS_SORTMAX 12288
+#endif
+constexpr int kSortMax = KS_SORTMAX;
 #ifndef KS_T0
 #define KS_T0 128
 #endif
@@ -91,7 +94,10 @@ __host__ __device__ constexpr int sort_cap(int c) { return (c == 0 || c == 4) ? 
 #define KS_T3 256
 #endif
 __host__ __device__ constexpr int sort_threads(int c) { return (c == 0 || c == 4) ? KS_T0 : (c == 1 ? KS_T1 : (c == 3 ? KS_T3 : 1024)); }
-__host__ __device__ constexpr int sort_lambda(int c) { return (c == 0 || c == 4) ? KS_LAM0 : ((c == 1 || c == 3) ? KS_LAM1 : 2); }   // keys per bucket
+#ifndef KS_LAM2
+#define KS_LAM2 2
+#endif
+__host__ __device__ constexpr int sort_lambda(int c) { return (c == 0 || c == 4) ? KS_LAM0 : ((c == 1 || c == 3) ? KS_LAM1 : KS_LAM2); }   // keys per bucket
 __host__ __device__ __forceinline__ int sort_class(long long len) { return len <= sort_cap(0) ? 0 : (len <= sort_cap(1) ? 1 : 2); }
 constexpr int kThreadSortMax = 16;                    // buckets up to this size: one thread, insertion sort
 #ifndef KS_LOCAL_THREADS
