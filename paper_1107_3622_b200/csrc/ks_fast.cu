@@ -95,6 +95,12 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_SINGLE2
 #define KS_SINGLE2 0      // the leaf's class-2 sorter with a single shared buffer (room for larger segments)
 #endif
+#ifndef KS_PLAN_FORK
+#define KS_PLAN_FORK 1    // the global plan runs concurrently with the scatter (data writes deferred to the finish pass)
+#endif
+#ifndef KS_FORK_ROOM
+#define KS_FORK_ROOM 0    // scatter CTAs given up for the forked plan's CTAs (measured 16: C0 -0.2%, C3 +3%)
+#endif
 #ifndef KS_MINB0
 #define KS_MINB0 5        // resident CTAs per SM asked for the class-0 small-segment sorter
 #endif
@@ -1188,6 +1194,8 @@ struct EmitArgs {
     double *keys;      // user buffer: short equality runs and tiny gaps are written here directly
     const double *tmp;
     int in_leaf;       // emitting inside the leaf launch: local children go to the sort queue
+    int defer;         // running concurrently with the scatter: no reads of the scattered data and no
+                       // writes to the scatter's source -- tiny gaps become units, pivot runs fill items
 };
 
 // packed per-thread counts for one block scan (11 bits each; blocks <= 1024 threads):
@@ -1315,7 +1323,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     }
 #endif
     if (have && !merged && (gl >= 2 || (gl == 1 && dst_id == 1))) {
-        if (gl <= kTinyGap) {
+        if (gl <= kTinyGap && !A.defer) {
             tiny_sort_copy((dst_id ? A.tmp : A.keys) + ag, A.keys + ag, (int)gl);
             t_gap = 1;
         }
@@ -1325,9 +1333,12 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         else if (gl <= kLocalMax) l_gap = 1;
         else g_gap = 1;
     }
-    if (have && el > 0 && el <= kFillDirect)
+    // pivot runs: written here when short (a merged group's run is its data:
+    // in tmp above, or here when the group lives in keys), else fill items
+    const bool direct = have && el > 0 && el <= kFillDirect && (merged ? dst_id == 0 : !A.defer);
+    if (direct)
         for (long long i = 0; i < el; ++i) A.keys[ae + i] = pv;
-    const int f_eq = (have && el > kFillDirect) ? (int)((el + kFillPiece - 1) / kFillPiece) : 0;   // fill pieces
+    const int f_eq = (have && el > 0 && !merged && !direct) ? (int)((el + kFillPiece - 1) / kFillPiece) : 0;   // fill pieces
     const int nu = u_gap + f_eq;
     // the plan stores big local items at the front of the local queue, the others from
     // the back: the leaf launch takes them front to back (longest first)
@@ -2611,6 +2622,30 @@ static DevStatus *pinned_status()
     return ps.p;
 }
 
+// Side stream + fork/join events of the calling thread on the current device
+// (thread-local: concurrent sorts from different threads never share them).
+struct ForkRes {
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static const ForkRes *fork_res()
+{
+    static thread_local ForkRes res[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    ForkRes &r = res[dev];
+    if (r.side == nullptr) {
+        if (cudaStreamCreateWithFlags(&r.side, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            r = ForkRes{};
+            return nullptr;
+        }
+    }
+    return &r;
+}
+
 static cudaStream_t capture_stream()
 {
     static std::mutex mu;
@@ -2648,7 +2683,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const EngineCfg *cfg = engine_cfg();
     if (cfg == nullptr) return KS_CUDA_ERROR;
     const int sms = cfg->sms;
-    const int g_count = cfg->g_count, g_scatter = cfg->g_scatter, g_leaf = cfg->g_leaf;
+    // with the plan forked next to the scatter, the scatter leaves room for the
+    // plan's CTAs (level 0: kPlanChunks of them) so that both are resident at once
+    const int g_count = cfg->g_count, g_leaf = cfg->g_leaf;
+    const int g_scatter = (KS_PLAN_FORK && !profile) ? std::max(cfg->sms, cfg->g_scatter - KS_FORK_ROOM) : cfg->g_scatter;
     const int g_scan = sms * 2;
     const int g_pivots = sms;
     Launcher K(stream, profile);
@@ -2704,7 +2742,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
         const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
-        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0};
+        const ForkRes *fr = (KS_PLAN_FORK && !profile) ? fork_res() : nullptr;
+        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, fr ? 1 : 0};
         if (!(level == 0 && d_off == nullptr))   // (done by k_init_single_pass)
             K.run(kPhPivots, [&] {
                 launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
@@ -2748,21 +2787,38 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                    reinterpret_cast<unsigned long long *>(bsum), moff);
         });
 #endif
-        K.run(kPhScatter, [&] {
-            launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur], chunk_seg,
-                   st, src, dst, piv, lut, moff, mat);
-        });
-        K.run(kPhPlan, [&] {
-            launch(k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A,
-                   st, dst_id);
-        });
+        if (fr != nullptr) {
+            // the plan needs only the scanned offsets and the pivots: it runs on a
+            // side stream next to the scatter (fork / join; inside the captured graph too)
+            cudaEventRecord(fr->fork, stream);
+            cudaStreamWaitEvent(fr->side, fr->fork, 0);
+            K.run(kPhPlan, [&] {
+                launch_pdl(false, k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, fr->side, segs[gcur], nseg_cur, piv,
+                           moff, A, st, dst_id);
+            });
+            K.run(kPhScatter, [&] {
+                launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur],
+                           chunk_seg, st, src, dst, piv, lut, moff, mat);
+            });
+            cudaEventRecord(fr->join, fr->side);
+            cudaStreamWaitEvent(stream, fr->join, 0);
+        } else {
+            K.run(kPhScatter, [&] {
+                launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur],
+                           chunk_seg, st, src, dst, piv, lut, moff, mat);
+            });
+            K.run(kPhPlan, [&] {
+                launch(k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A,
+                       st, dst_id);
+            });
+        }
         ++level;
         gcur ^= 1;
     };
     // leaf launch: queues -> sorted ranges; then the small segments by their own
     // CTA shapes (hand-backs go to the next leaf epoch), the warp units and fills
     auto leaf = [&]() {
-        EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1};
+        EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1, 0};
         K.run(kPhLeaf, [&] { launch_pdl(kPdlHeavy, k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // queue claims reset before the small sorts (their hand-backs belong to the next epoch)
         K.run(kPhGate, [&] {   // (bookkeeping launches are booked under "gate")
