@@ -641,13 +641,10 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *
 constexpr int kRankThreads = 128;
 constexpr int kRankParts = 8;   // threads per ranked key (a power of two dividing 32)
 
-__global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const Seg *segs, const double *src, double *sorted)
+__global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const double *in, int P, double *sorted)
 {
     KS_PDL_ENTRY();
     __shared__ double x[kPMax + 1];
-    const Seg g = segs[0];
-    const int P = g.P;
-    const double *in = src + g.start;
     constexpr int kU = (kPMax + 1 + kRankThreads - 1) / kRankThreads;   // all loads in flight at once
     double t[kU];
 #pragma unroll
@@ -2703,6 +2700,16 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
 
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
+    // level 0 of one array: its first P keys ranked into `sorted` (scratch in the
+    // offsets array, written only later by the scan)
+    bool rank_done = false;
+    auto launch_rank = [&](cudaStream_t s) {
+        const int P0 = pivots_for(n, kPMax);
+        K.run(kPhPivots, [&] {
+            launch_pdl(s == stream, k_pivot_rank, dim3((P0 * kRankParts + kRankThreads - 1) / kRankThreads),
+                       dim3(kRankThreads), 0, s, keys, P0, reinterpret_cast<double *>(moff));
+        });
+    };
     auto init_launch = [&]() {
         // queue ready words: cleared once per call (their tags carry the leaf epoch)
         cudaMemsetAsync(Q.lq_ready, 0, L.o_lq - L.o_lq_ready, stream);
@@ -2711,13 +2718,25 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream);
         }
         if (d_off == nullptr) {
-            if (n > kInitLocalMax)   // (+ the level-0 pass bookkeeping)
+            if (n > kInitLocalMax) {   // (+ the level-0 pass bookkeeping)
+                // the level-0 pivot ranking needs only the input: forked next to the init kernel
+                const ForkRes *fr = (KS_PLAN_FORK && !profile) ? fork_res() : nullptr;
+                if (fr != nullptr) {
+                    cudaEventRecord(fr->fork, stream);
+                    cudaStreamWaitEvent(fr->side, fr->fork, 0);
+                    launch_rank(fr->side);
+                }
                 K.run(kPhGate, [&] {
                     launch(k_init_single_pass, dim3(1), dim3(1024), 0, stream, n, Lst, st, L.mat_cap, L.ch_cap,
                            L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum),
                            std::min(g_count, g_scatter));
                 });
-            else
+                if (fr != nullptr) {
+                    cudaEventRecord(fr->join, fr->side);
+                    cudaStreamWaitEvent(stream, fr->join, 0);
+                    rank_done = true;
+                }
+            } else
                 K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
             if (n <= kInitLocalMax)
                 K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
@@ -2751,12 +2770,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                        std::min(g_count, g_scatter));
             });
         if (level == 0 && d_off == nullptr) {   // one segment, known P: build the pivots GPU-wide
-            const int P0 = pivots_for(n, kPMax);
             double *sorted = reinterpret_cast<double *>(moff);   // (scratch: the offsets are written later)
-            K.run(kPhPivots, [&] {
-                launch(k_pivot_rank, dim3((P0 * kRankParts + kRankThreads - 1) / kRankThreads), dim3(kRankThreads), 0,
-                       stream, segs[gcur], src, sorted);
-            });
+            if (!rank_done) launch_rank(stream);
             K.run(kPhPivots, [&] {
                 launch(k_pivot_lut, dim3(kLutCtas), dim3(kPivotThreads), 0, stream, segs[gcur], sorted, piv, lut,
                        chunk_seg, mat);
