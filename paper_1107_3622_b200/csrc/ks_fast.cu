@@ -98,6 +98,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_PLAN_FORK
 #define KS_PLAN_FORK 1    // the global plan runs concurrently with the scatter (data writes deferred to the finish pass)
 #endif
+#ifndef KS_SORT_FORK
+#define KS_SORT_FORK 1    // class-0 and class-1 list sorters run concurrently (side stream)
+#endif
 #ifndef KS_FORK_ROOM
 #define KS_FORK_ROOM 0    // scatter CTAs given up for the forked plan's CTAs (measured 16: C0 -0.2%, C3 +3%)
 #endif
@@ -2847,6 +2850,19 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         // single-buffer sorter (3 per SM, 256 threads) has the higher throughput;
         // on smaller ones the 512-thread sorter's shorter per-segment latency wins
         // (measured: 10M keys -2.4%, 500 x 100K -4.0%; 7M +4.4%, 1M +10%)
+        // the two lists are disjoint ranges: the class-0 sorter (which also finishes
+        // the warp units and fills) runs on the side stream next to the class-1
+        // sorter and fills the SMs the class-1 launch's tail leaves idle
+        // (measured: 100K keys -12%, 500 x 100K -2.3%; one array of 10M keys +1.8%
+        // -- there the class-1 list alone fills the GPU -- so not for large arrays)
+        const bool sort_fork = KS_SORT_FORK && !profile && (n < KS_SINGLE_MIN_N || d_off != nullptr);
+        const ForkRes *fr = sort_fork ? fork_res() : nullptr;
+        cudaStream_t s0 = stream;
+        if (fr != nullptr) {
+            cudaEventRecord(fr->fork, stream);
+            cudaStreamWaitEvent(fr->side, fr->fork, 0);
+            s0 = fr->side;
+        }
         if (n >= KS_SINGLE_MIN_N)
             K.run(kPhLeaf, [&] {
                 launch_pdl(kPdlHeavy, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sizeof(SortSmem<3>), stream,
@@ -2859,14 +2875,20 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             });
         if (n >= KS_SINGLE_MIN_N)   // (same trade-off for the class-0 list: 8 single-buffer sorters per SM)
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)), sizeof(SortSmem<4>), stream,
-                           Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
+                launch_pdl(kPdlHeavy && s0 == stream, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)),
+                           sizeof(SortSmem<4>), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
+                           units);
             });
         else
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sizeof(SortSmem<0>), stream,
-                           Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp, units);
+                launch_pdl(kPdlHeavy && s0 == stream, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)),
+                           sizeof(SortSmem<0>), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
+                           units);
             });
+        if (fr != nullptr) {
+            cudaEventRecord(fr->join, fr->side);
+            cudaStreamWaitEvent(stream, fr->join, 0);
+        }
         K.run(kPhGate, [&] {
             launch(k_set_ints, dim3(1), dim3(32), 0, stream,
                    IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,
