@@ -48,7 +48,19 @@ __device__ unsigned long long g_trace[32];
 
 // build-time variants (experiments; defaults are the measured best)
 #ifndef KS_BATCH
-#define KS_BATCH 0        // batched (overlapped) classify in the count / scatter loops (measured: no gain)
+#define KS_BATCH 0        // batched (overlapped) classify in the count / scatter loops: 1 = all U keys at once
+#endif                    // (measured: no gain, spills at 40 registers), 2 = groups of KS_BATCH_G keys
+#ifndef KS_SRC_CS
+#define KS_SRC_CS 1       // 1: the scatter's source loads are evict-first (ld.global.cs): C0 -3..5%
+#endif
+#ifndef KS_PF_MIN_N
+#define KS_PF_MIN_N 2500000   // scatter destinations are prefetched into L2 for calls of at least this many keys
+#endif                        // (measured: 1M/2M keys -9%/-6% without, 3M..10M +6..11% without)
+#ifndef KS_ITEM_PF_MIN_N
+#define KS_ITEM_PF_MIN_N 2500000   // the small-segment sorters prefetch their next item into L2 for calls of at
+#endif                             // least this many keys (measured without: 1M -9%, 2M -6%; 3M..10M +6..11%)
+#ifndef KS_BATCH_G
+#define KS_BATCH_G 4
 #endif
 #ifndef KS_SCATTER_EXP
 #define KS_SCATTER_EXP 0
@@ -292,6 +304,7 @@ __global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
     __syncthreads();
     if (threadIdx.x != 0) return;
     st->bad_index = kNoIndex;
+    st->no_item_pf = n < KS_ITEM_PF_MIN_N ? 1 : 0;
     route_initial(0, n, Lst, st);
 }
 
@@ -590,6 +603,7 @@ __global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, lo
     __syncthreads();
     if (threadIdx.x == 0) {
         st->bad_index = kNoIndex;
+        st->no_item_pf = n < KS_ITEM_PF_MIN_N ? 1 : 0;
         route_initial(0, n, Lst, st);
     }
     __syncthreads();
@@ -834,7 +848,15 @@ __global__ void __launch_bounds__(kCountThreads, KS_PASS_MINB) k_count(const Seg
                     for (int u = 0; u < U; ++u) gate_one(v[u], base + threadIdx.x + i0 + u * kCountThreads, bad, pz, nz);
                 }
             }
-#if KS_BATCH
+#if KS_BATCH == 2
+#pragma unroll
+            for (int g0 = 0; g0 < U; g0 += KS_BATCH_G) {
+                int c[KS_BATCH_G];
+                classify_batch<KS_BATCH_G>(v + g0, c, P.piv, P.lut, lo, scale, T);
+#pragma unroll
+                for (int u = 0; u < KS_BATCH_G; ++u) atomicAdd(&hist[c[u]], 1u);
+            }
+#elif KS_BATCH
             int c[U];
             classify_batch<U>(v, c, P.piv, P.lut, lo, scale, T);
 #pragma unroll
@@ -1059,6 +1081,19 @@ __device__ __forceinline__ void scatter_store(double *p, double v)
 #endif
 }
 
+#ifndef KS_OUT_HINT
+#define KS_OUT_HINT 0     // cache hint of the segment sorters' final stores (0 default, 1 .cs evict-first)
+#endif
+// final sorted keys: never read again by the sort
+__device__ __forceinline__ void out_store(double *p, double v)
+{
+#if KS_OUT_HINT == 1
+    __stcs(p, v);
+#else
+    *p = v;
+#endif
+}
+
 struct ScatterSmem {
     PassSmem P;
     unsigned cursor[kPMax + 1];   // next slot per gap class, relative to the segment start
@@ -1068,7 +1103,7 @@ struct ScatterSmem {
 __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Seg *segs, const int *chunk_seg,
                                                           const DevStatus *cst, const double *src, double *dst,
                                                           const double *piv_pool, const unsigned *lut_pool,
-                                                          const long long *moff, const unsigned *mat)
+                                                          const long long *moff, const unsigned *mat, int pf)
 {
     KS_PDL_ENTRY();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1110,8 +1145,9 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
                     S.cursor[q] = c0;
 #if KS_PREFETCH
                     // pull this chunk's destination run of gap q into L2 ahead of the
-                    // 8-byte stores (a partial-sector store that misses L2 waits for a fill)
-                    l2_prefetch_lines(out + c0, 8ull * cnt[u]);
+                    // 8-byte stores (a partial-sector store that misses L2 waits for a fill);
+                    // not when the whole pass is L2-resident anyway (pf == 0)
+                    if (pf) l2_prefetch_lines(out + c0, 8ull * cnt[u]);
 #endif
                 }
             }
@@ -1122,8 +1158,24 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
         for (; i0 + U * kPassThreads <= cnt; i0 += U * kPassThreads) {
             double v[U];
 #pragma unroll
+#if KS_SRC_CS   // last read of the source at this level: evict-first, so the prefetched destination stays
+            for (int u = 0; u < U; ++u) v[u] = __ldcs(in + i0 + u * kPassThreads);
+#else
             for (int u = 0; u < U; ++u) v[u] = in[i0 + u * kPassThreads];
-#if KS_BATCH
+#endif
+#if KS_BATCH == 2
+#pragma unroll
+            for (int g0 = 0; g0 < U; g0 += KS_BATCH_G) {
+                int c[KS_BATCH_G];
+                classify_batch<KS_BATCH_G>(v + g0, c, S.P.piv, S.P.lut, lo, scale, T);
+                unsigned slot[KS_BATCH_G];
+#pragma unroll
+                for (int u = 0; u < KS_BATCH_G; ++u) slot[u] = (c[u] & 1) ? 0u : atomicAdd(&S.cursor[c[u] >> 1], 1u);
+#pragma unroll
+                for (int u = 0; u < KS_BATCH_G; ++u)
+                    if (!(c[u] & 1)) scatter_store(out + slot[u], v[g0 + u]);
+            }
+#elif KS_BATCH
             int c[U];
             classify_batch<U>(v, c, S.P.piv, S.P.lut, lo, scale, T);
             unsigned slot[U];
@@ -1793,6 +1845,7 @@ struct SegFeed {
     int *sidx;
     const double *keys, *tmp;
     bool done;
+    bool pf;         // per-item L2 prefetches (off for small, L2-resident calls)
     __device__ __forceinline__ void after_load()
     {
         if (threadIdx.x != 0) return;
@@ -1814,6 +1867,7 @@ struct SegFeed {
         if (threadIdx.x != 0 || d >= n) return;
         asm volatile("cp.async.wait_all;" ::: "memory");
 #if KS_PREFETCH
+        if (!pf) return;
         const Seg &g = *slot;
         l2_prefetch((g.src ? tmp : keys) + g.start, 8ull * g.len);
         if (g.src) l2_prefetch(keys + g.start, 8ull * g.len);
@@ -1953,7 +2007,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     if (scale < 0.0) {   // constant segment: already sorted
         if (g.src) {
 #pragma unroll 1
-            for (int i = tid; i < m; i += kT) out[i] = Smem::kSingle ? __ldcg(in + i) : S.a[i];
+            for (int i = tid; i < m; i += kT) out_store(out + (i), Smem::kSingle ? __ldcg(in + i) : S.a[i]);
         }
         feed.after_scatter();
     } else {
@@ -2039,7 +2093,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 }
                 pos = r;
             }
-            out[pos] = x;
+            out_store(out + (pos), x);
         }
 #else
         // 4a. one thread per bucket: <= 4 keys -> sorting network in registers,
@@ -2063,7 +2117,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                         mid[q] = b;
                     } else {   // list full: the owner sorts it
                         smem_insertion_sort(S.b + s0, sz);
-                        for (int i = 0; i < sz; ++i) out[s0 + i] = S.b[s0 + i];
+                        for (int i = 0; i < sz; ++i) out_store(out + (s0 + i), S.b[s0 + i]);
                     }
                     continue;
                 }
@@ -2103,7 +2157,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                     const double y = x[j];
                     r += (y < v || (y == v && j < l)) ? 1 : 0;
                 }
-                out[s0 + r] = v;
+                out_store(out + (s0 + r), v);
             }
         }
 #else
@@ -2113,7 +2167,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             const int s0 = b ? (int)S.cur[b - 1] : 0;
             const int sz = (int)S.cur[b] - s0;
             smem_insertion_sort(S.b + s0, sz);
-            for (int i = 0; i < sz; ++i) out[s0 + i] = S.b[s0 + i];
+            for (int i = 0; i < sz; ++i) out_store(out + (s0 + i), S.b[s0 + i]);
         }
 #endif
         // 4c. large buckets (sorted by warps above, or handed back): coalesced copy
@@ -2121,7 +2175,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             const int b = S.big[q];
             const int s0 = b ? (int)S.cur[b - 1] : 0;
             const int sz = (int)S.cur[b] - s0;
-            for (int i = lane; i < sz; i += 32) out[s0 + i] = S.b[s0 + i];
+            for (int i = lane; i < sz; i += 32) out_store(out + (s0 + i), S.b[s0 + i]);
         }
 #endif
         // hand-backs are published only once their keys are in place
@@ -2158,9 +2212,10 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
     // thread 0 claims one item ahead and pulls its input and output ranges into
     // L2 while the current one is sorted (a cold segment otherwise costs two
     // DRAM round trips to load and a fill stall per partially written sector)
+    const bool pf = !st->no_item_pf;
     auto prefetch = [&](int d) {
 #if KS_PREFETCH
-        if (d < n) {
+        if (d < n && pf) {
             const Seg g = list[d];
             l2_prefetch((g.src ? tmp : keys) + g.start, 8ull * g.len);
             if (g.src) l2_prefetch(keys + g.start, 8ull * g.len);
@@ -2184,7 +2239,7 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         __syncthreads();
         if (s_idx[slot] >= n) break;
         const Seg g = s_seg[slot];
-        SegFeed f{list, n, 0, &s_seg[slot ^ 1], &s_idx[slot ^ 1], keys, tmp, false};
+        SegFeed f{list, n, 0, &s_seg[slot ^ 1], &s_idx[slot ^ 1], keys, tmp, false, pf};
         if (threadIdx.x == 0) f.d = atomicAdd(next, 1);   // (used after the load phase)
         segsort_one<C>(S, g, Q, st, keys, tmp, f);
         f.after_scatter();   // (no-op unless the segment took no scatter path)
@@ -2755,6 +2810,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // the end; inputs that need more global passes (adversarial shapes:
     // presorted, few distinct values, ...) continue in a synchronising loop.
     int level = 0, gcur = 0, leaves_run = 0;
+    const int scatter_pf = n >= KS_PF_MIN_N ? 1 : 0;
     auto global_pass = [&]() {
         const double *src = (level & 1) ? tmp : keys;
         double *dst = (level & 1) ? keys : tmp;
@@ -2816,14 +2872,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             });
             K.run(kPhScatter, [&] {
                 launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur],
-                           chunk_seg, st, src, dst, piv, lut, moff, mat);
+                           chunk_seg, st, src, dst, piv, lut, moff, mat, scatter_pf);
             });
             cudaEventRecord(fr->join, fr->side);
             cudaStreamWaitEvent(stream, fr->join, 0);
         } else {
             K.run(kPhScatter, [&] {
                 launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur],
-                           chunk_seg, st, src, dst, piv, lut, moff, mat);
+                           chunk_seg, st, src, dst, piv, lut, moff, mat, scatter_pf);
             });
             K.run(kPhPlan, [&] {
                 launch(k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A,

@@ -131,6 +131,8 @@ struct DevStatus {
     int nchunks;                      // chunks of the current level
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
+    int no_item_pf;                   // small call: the sorters' per-item L2 prefetches are skipped
+    int pad_;
     int scan_next;                    // tile counter of the single-pass count-matrix scan
     int chunk;                        // keys per chunk of the current level
     unsigned long long bytes_moved;   // algorithmic bytes, all passes
@@ -287,7 +289,7 @@ __device__ __forceinline__ int classify(double v, const double *piv, const unsig
 // then branch-free class arithmetic.  Buckets with more than two pivots
 // (rare when T >= 4P) are finished by the general classify.
 template <int U>
-__device__ __forceinline__ void classify_batch(const double (&v)[U], int (&c)[U], const double *piv,
+__device__ __forceinline__ void classify_batch(const double *v, int *c, const double *piv,
                                                const unsigned *lut, double lo, double scale, int T)
 {
     unsigned e[U];
@@ -334,13 +336,21 @@ __device__ __forceinline__ void l2_prefetch(const void *p, unsigned long long by
 // Per-thread L2 prefetch of the 128-byte lines covering [p, p + bytes): a plain
 // (non-uniform) instruction per line, for many small ranges at once -- the
 // bulk form takes a uniform operand and serialises across the lanes of a warp.
+#ifndef KS_PF_EVL
+#define KS_PF_EVL 0   // 1: the scatter's destination prefetches are marked evict-last in L2
+#endif
 __device__ __forceinline__ void l2_prefetch_lines(const void *p, unsigned long long bytes)
 {
     if (bytes == 0) return;
     const unsigned long long a0 = reinterpret_cast<unsigned long long>(p) & ~127ull;
     const unsigned long long a1 = reinterpret_cast<unsigned long long>(p) + bytes;
-    for (unsigned long long a = a0; a < a1; a += 128)
+    for (unsigned long long a = a0; a < a1; a += 128) {
+#if KS_PF_EVL
+        asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(a) : "memory");
+#else
         asm volatile("prefetch.global.L2 [%0];" ::"l"(a) : "memory");
+#endif
+    }
 }
 
 __host__ __device__ __forceinline__ long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
