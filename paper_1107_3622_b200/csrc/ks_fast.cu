@@ -1094,6 +1094,29 @@ __device__ __forceinline__ void out_store(double *p, double v)
 #endif
 }
 
+#ifndef KS_LOCAL_CS
+#define KS_LOCAL_CS 0     // 1: the local partition's scatter loads (last read of its source) are evict-first
+#endif
+#ifndef KS_SEG_CS
+#define KS_SEG_CS 0       // 1: the two-buffer segment sorters' loads (last read of the segment) are evict-first
+#endif
+__device__ __forceinline__ double ld_local_last(const double *p)
+{
+#if KS_LOCAL_CS
+    return __ldcs(p);
+#else
+    return __ldcg(p);
+#endif
+}
+template <bool kSingle>
+__device__ __forceinline__ double ld_seg(const double *p)
+{
+#if KS_SEG_CS
+    if (!kSingle) return __ldcs(p);
+#endif
+    return __ldcg(p);
+}
+
 struct ScatterSmem {
     PassSmem P;
     unsigned cursor[kPMax + 1];   // next slot per gap class, relative to the segment start
@@ -1579,7 +1602,7 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
     for (; i0 + U * kLocalThreads <= m; i0 += U * kLocalThreads) {
         double v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcg(src + i0 + u * kLocalThreads + threadIdx.x);
+        for (int u = 0; u < U; ++u) v[u] = ld_local_last(src + i0 + u * kLocalThreads + threadIdx.x);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int c = classify(v[u], L.piv, L.lut, lo, scale, T);
@@ -1587,7 +1610,7 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
         }
     }
     for (int i = i0 + threadIdx.x; i < m; i += kLocalThreads) {
-        const double v = __ldcg(src + i);
+        const double v = ld_local_last(src + i);
         const int c = classify(v, L.piv, L.lut, lo, scale, T);
         if (!(c & 1)) dst[atomicAdd(&L.cursor[c], 1u)] = v;
     }
@@ -1925,7 +1948,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 #pragma unroll
             for (int u = 0; u < kLU; ++u) {
                 const int i = i0 + u * kT + tid;
-                x[u] = i < m ? __ldcg(in + i) : 0.0;
+                x[u] = i < m ? ld_seg<Smem::kSingle>(in + i) : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < kLU; ++u) {
@@ -1944,7 +1967,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 #pragma unroll
         for (int u = 0; u < kLU; ++u) {
             const int i = i0 + u * kT + tid;
-            x[u] = i < m ? __ldcg(in + i) : 0.0;
+            x[u] = i < m ? ld_seg<Smem::kSingle>(in + i) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < kLU; ++u) {
