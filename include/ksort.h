@@ -73,6 +73,16 @@ size_t ks_workspace_bytes(int64_t n_total, int64_t n_segments, uint32_t flags);
 int ks_sort_f64(double *d_keys, int64_t n, void *d_ws, size_t ws_bytes, void *stream,
                 uint32_t flags, ks_status_t *h_status);
 
+/* Replaces sort_core.k_sort (sort_core.py:169-217) on a HOST array: h_keys[0..n)
+ * is copied to the device buffer d_keys (n doubles, caller-allocated), sorted
+ * there and copied back into h_keys, all on `stream` with one synchronisation
+ * (the copy back is queued behind the sort before the status is read, so the
+ * device never waits for the host between the three steps).  Pinned h_keys
+ * gives asynchronous copies.  On any error h_keys keeps its bytes.  Same
+ * flags, codes and status as ks_sort_f64. */
+int ks_sort_f64_host(double *h_keys, int64_t n, double *d_keys, void *d_ws, size_t ws_bytes, void *stream,
+                     uint32_t flags, ks_status_t *h_status);
+
 /* Batch entry (new API; the reference bench calls k_sort once per array,
  * bench.py:169-173): sort each segment d_keys[off[s]..off[s+1]) independently,
  * exactly as k_sort would sort it.  d_offsets: device int64[n_segments+1],

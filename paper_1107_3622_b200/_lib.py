@@ -25,7 +25,7 @@ KS_FLAG_PROFILE = 4
 PHASES = ("gate", "pivots", "count", "scan", "scatter", "plan", "leaf", "local")
 
 EXPORTED = (
-    "ks_workspace_bytes", "ks_sort_f64", "ks_sort_f64_segmented", "ks_partition_f64",
+    "ks_workspace_bytes", "ks_sort_f64", "ks_sort_f64_host", "ks_sort_f64_segmented", "ks_partition_f64",
     "ks_heap_sort_f64_exact", "ks_is_sorted_f64", "ks_first_nonfinite_f64", "ks_generate_f64", "ks_version",
 )
 
@@ -77,6 +77,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.ks_workspace_bytes.restype = sz
     L.ks_sort_f64.argtypes = [vp, i64, vp, sz, vp, u32, st]
     L.ks_sort_f64.restype = ctypes.c_int
+    L.ks_sort_f64_host.argtypes = [vp, i64, vp, vp, sz, vp, u32, st]
+    L.ks_sort_f64_host.restype = ctypes.c_int
     L.ks_sort_f64_segmented.argtypes = [vp, vp, i64, i64, vp, sz, vp, u32, st]
     L.ks_sort_f64_segmented.restype = ctypes.c_int
     L.ks_partition_f64.argtypes = [vp, i64, i64, i64, vp, sz, vp, ctypes.POINTER(i64),

@@ -119,6 +119,47 @@ int ks_sort_f64(double *d_keys, int64_t n, void *d_ws, size_t ws_bytes, void *st
     return s->code = KS_OK;
 }
 
+int ks_sort_f64_host(double *h_keys, int64_t n, double *d_keys, void *d_ws, size_t ws_bytes, void *stream,
+                     uint32_t flags, ks_status_t *h_status)
+{
+    ks_status_t local;
+    ks_status_t *s = h_status ? h_status : &local;
+    status_init(s);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (n < 0 || (n > 0 && (d_keys == nullptr || h_keys == nullptr))) return s->code = KS_BAD_ARG;
+    if (n == 0) return s->code = KS_OK;
+    const size_t bytes = 8ull * (size_t)n;
+    if (cudaMemcpyAsync(d_keys, h_keys, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return s->code = KS_CUDA_ERROR;
+    auto copy_back = [&]() -> int {
+        if (cudaMemcpyAsync(h_keys, d_keys, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+            cudaStreamSynchronize(st) != cudaSuccess)
+            return KS_CUDA_ERROR;
+        return KS_OK;
+    };
+    if (flags & KS_FLAG_COUNTS) flags |= KS_FLAG_EXACT;
+    if (flags & KS_FLAG_EXACT) {
+        int rc = run_exact(d_keys, n, d_ws, ws_bytes, st, (flags & KS_FLAG_COUNTS) != 0, s);
+        if (rc == KS_OK) rc = copy_back();
+        return s->code = rc;
+    }
+    FastResult r{};
+    int rc = fast_sort(d_keys, n, nullptr, 1, d_ws, ws_bytes, st, (flags & KS_FLAG_PROFILE) != 0, &r, h_keys);
+    if (rc != KS_OK) return s->code = rc;
+    if (r.bad_index >= 0) {
+        fill_bad(s, d_keys, r.bad_index, st);
+        return s->code;
+    }
+    if (r.mixed_zero) {
+        if (ws_bytes < exact_bytes(n, false)) return s->code = KS_NEED_EXACT;
+        rc = run_exact(d_keys, n, d_ws, ws_bytes, st, false, s);
+        if (rc == KS_OK) rc = copy_back();
+        return s->code = rc;
+    }
+    copy_fast(s, r);
+    return s->code = KS_OK;
+}
+
 int ks_sort_f64_segmented(double *d_keys, const int64_t *d_offsets, int64_t n_segments, int64_t n_total,
                           void *d_ws, size_t ws_bytes, void *stream, uint32_t flags, ks_status_t *h_status)
 {

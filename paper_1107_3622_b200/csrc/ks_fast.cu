@@ -2737,7 +2737,7 @@ static cudaStream_t capture_stream()
 }
 
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
-              cudaStream_t user_stream, bool profile, FastResult *res)
+              cudaStream_t user_stream, bool profile, FastResult *res, double *h_out)
 {
     cudaStream_t stream = user_stream;   // (the capture stream while a graph is being recorded)
     FastLayout L = fast_layout(n, nseg0);
@@ -3024,14 +3024,23 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         }
     }
     if (!replayed) spec();
+    // host destination: copied behind the speculative schedule (an aborted sort
+    // wrote nothing, so the copy returns the caller's own bytes)
+    if (h_out != nullptr && n > 0) KS_CK(cudaMemcpyAsync(h_out, keys, 8ull * n, cudaMemcpyDeviceToHost, stream));
     int rc = sync_status();
     if (rc != KS_OK) return rc;
     // remaining work (rare): more global levels, or hand-backs queued for another leaf launch
+    bool more = false;
     while (!aborted() && (h.nseg[gcur] > 0 || h.sq_claim > 0 || h.lq_claim > 0 || h.lqb_claim > 0)) {
         if (h.nseg[gcur] > 0) global_pass();
         leaf();
+        more = true;
         rc = sync_status();
         if (rc != KS_OK) return rc;
+    }
+    if (more && h_out != nullptr) {
+        KS_CK(cudaMemcpyAsync(h_out, keys, 8ull * n, cudaMemcpyDeviceToHost, stream));
+        KS_CK(cudaStreamSynchronize(stream));
     }
     res->levels = level + leaves_run;
     res->bad_index = h.bad_index == kNoIndex ? -1 : (long long)h.bad_index;

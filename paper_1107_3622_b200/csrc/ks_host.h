@@ -28,8 +28,10 @@ struct FastResult {
 };
 
 FastLayout fast_layout(long long n, long long nseg0);
+// h_out (optional): host destination of the sorted keys; the copy is queued
+// right behind the sort, before the status read (rewritten if more passes run)
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws,
-              size_t ws_bytes, cudaStream_t stream, bool profile, FastResult *res);
+              size_t ws_bytes, cudaStream_t stream, bool profile, FastResult *res, double *h_out = nullptr);
 
 }  // namespace ks
 

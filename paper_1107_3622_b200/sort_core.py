@@ -216,6 +216,44 @@ def _sort_device(keys: torch.Tensor, flags: int = 0) -> _lib.KsStatus:
     return st
 
 
+def _host_view(a: ArrayLike) -> Optional[torch.Tensor]:
+    """A CPU float64 tensor sharing the caller's memory (host tensors and
+    ndarrays that are contiguous 1-D float64), else None."""
+    if isinstance(a, torch.Tensor):
+        if a.is_cuda:
+            return None
+        if a.dtype != torch.float64 or a.dim() != 1:
+            raise TypeError("expected a 1-D float64 tensor")
+        return a if a.is_contiguous() and a.numel() > 0 else None
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.float64 or a.ndim != 1:
+            raise TypeError("expected a 1-D float64 array")
+        if a.size > 0 and a.flags.c_contiguous and a.flags.writeable:
+            return torch.from_numpy(a)
+    return None
+
+
+def _sort_host(h: torch.Tensor, flags: int = 0) -> _lib.KsStatus:
+    """Sort a host float64 tensor in place through ks_sort_f64_host (H2D, sort,
+    D2H queued on one stream; pinned memory makes the copies asynchronous)."""
+    L = _lib.load()
+    n = h.numel()
+    dev = torch.empty(n, dtype=torch.float64, device=_device())
+    st = _lib.KsStatus()
+    ws_bytes = _workspace_bytes(L, n, 1, flags)
+    ws = _workspace(ws_bytes)
+    code = L.ks_sort_f64_host(h.data_ptr(), n, dev.data_ptr(), ws.data_ptr(), ws_bytes, _stream_ptr(), flags,
+                              ctypes.byref(st))
+    if code == _lib.KS_NEED_EXACT:
+        ws_bytes = _workspace_bytes(L, n, 1, flags | _lib.KS_FLAG_EXACT)
+        ws = _workspace(ws_bytes)
+        code = L.ks_sort_f64_host(h.data_ptr(), n, dev.data_ptr(), ws.data_ptr(), ws_bytes, _stream_ptr(), flags,
+                                  ctypes.byref(st))
+    _raise_for(code, st, "k_sort")
+    _record(st)
+    return st
+
+
 # ---------------------------------------------------------------------------
 # reference API
 # ---------------------------------------------------------------------------
@@ -267,11 +305,17 @@ def k_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     With ``counts`` the exact engine runs and the reference's tallies are
     accumulated (comparisons/moves added, max_pending_ranges maxed).
     """
-    s = _Staged(a)
     flags = _lib.KS_FLAG_COUNTS if counts is not None else 0
-    st = _sort_device(s.dev, flags)
-    s.write_back()
-    if counts is not None and s.n >= 2:
+    h = _host_view(a)
+    if h is not None:   # host tensor / ndarray: copy in, sort, copy back with one synchronisation
+        n = h.numel()
+        st = _sort_host(h, flags)
+    else:
+        s = _Staged(a)
+        n = s.n
+        st = _sort_device(s.dev, flags)
+        s.write_back()
+    if counts is not None and n >= 2:
         counts.comparisons += int(st.comparisons)
         counts.moves += int(st.moves)
         counts.max_pending_ranges = max(counts.max_pending_ranges, int(st.max_pending_ranges))

@@ -281,6 +281,67 @@ def test_list_and_numpy_and_cpu_tensor_inputs():
     assert K.is_sorted(a) and K.is_sorted(c) and not K.is_sorted(base)
 
 
+# ---- host buffers through ks_sort_f64_host (H2D, sort, D2H with one synchronisation) ----
+
+def _host_inputs(base):
+    yield "numpy", base.copy()
+    yield "cpu", torch.from_numpy(base.copy())
+    yield "pinned", torch.from_numpy(base.copy()).pin_memory()
+
+
+def _bits(x):
+    return x.numpy() if isinstance(x, torch.Tensor) else x
+
+
+@pytest.mark.parametrize("n", [1, 2, 700, 20_000, 1_000_000, 3_000_000])
+def test_host_buffers_bitexact(n):
+    base = np.random.default_rng(n).random(n)
+    want = np.sort(base)
+    for name, x in _host_inputs(base):
+        K.k_sort(x)
+        assert same_bits(_bits(x), want), name
+
+
+@pytest.mark.parametrize("n", [5000, 100_000, 2_000_000])
+def test_host_buffers_nonfinite_untouched(n):
+    rng = np.random.default_rng(n + 7)
+    base = rng.random(n)
+    pos = int(rng.integers(0, n))
+    base[pos] = float("inf")
+    for name, x in _host_inputs(base):
+        with pytest.raises(K.NonFiniteKeyError) as ei:
+            K.k_sort(x)
+        assert str(ei.value) == f"key at index {pos} is inf; keys must be finite"
+        assert same_bits(_bits(x), base), name
+
+
+def test_host_buffers_signed_zeros_and_counts_match_oracle():
+    rng = np.random.default_rng(11)
+    base = rng.integers(-3, 4, size=50_000).astype(np.float64)
+    base[rng.integers(0, base.size, size=500)] = -0.0   # both zeros: the exact engine
+    want = oracle_ksort(base)
+    for name, x in _host_inputs(base):
+        K.k_sort(x)
+        assert same_bits(_bits(x), want), name
+    small = np.array(TRACE_ARRAY)
+    c = K.OpCounts()
+    K.k_sort(small, c)
+    assert small.tolist() == TRACE_SORTED and (c.comparisons, c.moves, c.max_pending_ranges) == (20, 26, 2)
+
+
+@pytest.mark.parametrize("kind", ["presorted", "few_distinct"])
+def test_host_buffers_multi_pass_inputs(kind):
+    # inputs that need the synchronising loop after the speculative schedule:
+    # the copy back is rewritten after the extra passes
+    n = 3_000_000
+    a = np.arange(n, dtype=np.float64) if kind == "presorted" else \
+        np.random.default_rng(5).integers(0, 3, size=n).astype(np.float64)
+    for name, x in _host_inputs(a):
+        K.k_sort(x)
+        assert same_bits(_bits(x), np.sort(a)), name
+        assert K.last_stats.levels >= 1
+
+
 # ---- adversarial shapes (forward progress + parity) ----------------------------------
 
 @pytest.mark.parametrize("kind", ["presorted", "reversed", "constant", "organ", "few_distinct"])
