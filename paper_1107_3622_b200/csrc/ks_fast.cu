@@ -59,6 +59,12 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_ITEM_PF_MIN_N
 #define KS_ITEM_PF_MIN_N 2500000   // the small-segment sorters prefetch their next item into L2 for calls of at
 #endif                             // least this many keys (measured without: 1M -9%, 2M -6%; 3M..10M +6..11%)
+#ifndef KS_SBATCH
+#define KS_SBATCH 0       // scatter: classify in groups of this many keys (LUT loads, pivot loads, atomics, stores)
+#endif
+#ifndef KS_SCAT_MINB
+#define KS_SCAT_MINB KS_PASS_MINB   // resident scatter CTAs per SM asked (2: 64 registers for the grouped classify)
+#endif
 #ifndef KS_BATCH_G
 #define KS_BATCH_G 4
 #endif
@@ -1123,7 +1129,7 @@ struct ScatterSmem {
     Seg sg;
 };
 
-__global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Seg *segs, const int *chunk_seg,
+__global__ void __launch_bounds__(kPassThreads, KS_SCAT_MINB) k_scatter(const Seg *segs, const int *chunk_seg,
                                                           const DevStatus *cst, const double *src, double *dst,
                                                           const double *piv_pool, const unsigned *lut_pool,
                                                           const long long *moff, const unsigned *mat, int pf)
@@ -1186,16 +1192,16 @@ __global__ void __launch_bounds__(kPassThreads, KS_PASS_MINB) k_scatter(const Se
 #else
             for (int u = 0; u < U; ++u) v[u] = in[i0 + u * kPassThreads];
 #endif
-#if KS_BATCH == 2
+#if KS_SBATCH
 #pragma unroll
-            for (int g0 = 0; g0 < U; g0 += KS_BATCH_G) {
-                int c[KS_BATCH_G];
-                classify_batch<KS_BATCH_G>(v + g0, c, S.P.piv, S.P.lut, lo, scale, T);
-                unsigned slot[KS_BATCH_G];
+            for (int g0 = 0; g0 < U; g0 += KS_SBATCH) {
+                int c[KS_SBATCH];
+                classify_batch<KS_SBATCH>(v + g0, c, S.P.piv, S.P.lut, lo, scale, T);
+                unsigned slot[KS_SBATCH];
 #pragma unroll
-                for (int u = 0; u < KS_BATCH_G; ++u) slot[u] = (c[u] & 1) ? 0u : atomicAdd(&S.cursor[c[u] >> 1], 1u);
+                for (int u = 0; u < KS_SBATCH; ++u) slot[u] = (c[u] & 1) ? 0u : atomicAdd(&S.cursor[c[u] >> 1], 1u);
 #pragma unroll
-                for (int u = 0; u < KS_BATCH_G; ++u)
+                for (int u = 0; u < KS_SBATCH; ++u)
                     if (!(c[u] & 1)) scatter_store(out + slot[u], v[g0 + u]);
             }
 #elif KS_BATCH
