@@ -65,6 +65,9 @@ __device__ unsigned long long g_trace[32];
 #ifndef KS_SCAT_MINB
 #define KS_SCAT_MINB KS_PASS_MINB   // resident scatter CTAs per SM asked (2: 64 registers for the grouped classify)
 #endif
+#ifndef KS_PF_EARLY
+#define KS_PF_EARLY 0     // 1: scatter CTAs issue their destination prefetches before copying the pivot tables
+#endif
 #ifndef KS_BATCH_G
 #define KS_BATCH_G 4
 #endif
@@ -767,11 +770,19 @@ struct PassSmem {
     unsigned lut[kLutMax];
 };
 
+__device__ __forceinline__ void load_seg_tables(const double *piv_pool, const unsigned *lut_pool, const Seg &sg,
+                                                PassSmem &P);
 __device__ __forceinline__ void load_seg(const Seg *segs, int s, const double *piv_pool, const unsigned *lut_pool,
                                          Seg &sg, PassSmem &P)
 {
     if (threadIdx.x == 0) sg = segs[s];
     __syncthreads();
+    load_seg_tables(piv_pool, lut_pool, sg, P);
+}
+// the segment's pivots and LUT into shared memory (descriptor already in sg)
+__device__ __forceinline__ void load_seg_tables(const double *piv_pool, const unsigned *lut_pool, const Seg &sg,
+                                                PassSmem &P)
+{
     // copies unrolled by 8 so that the L2 loads overlap (a rolled copy waits
     // one L2 round trip per element per thread)
     const int np = sg.k + kPivPad, T = sg.T;
@@ -1144,10 +1155,18 @@ __global__ void __launch_bounds__(kPassThreads, KS_SCAT_MINB) k_scatter(const Se
     for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
         const int s = chunk_seg[ch];
         __syncthreads();
+#if KS_PF_EARLY   // descriptor first, the cursors and destination prefetches next, the tables last
+        const bool fresh = s != cached;
+        if (fresh) {
+            if (threadIdx.x == 0) S.sg = segs[s];
+            __syncthreads();
+        }
+#else
         if (s != cached) {
             load_seg(segs, s, piv_pool, lut_pool, S.sg, S.P);
             cached = s;
         }
+#endif
         const Seg &g = S.sg;
         const int j = ch - g.ch_off;
         const long long base = g.start + (long long)j * chunk;
@@ -1181,6 +1200,12 @@ __global__ void __launch_bounds__(kPassThreads, KS_SCAT_MINB) k_scatter(const Se
                 }
             }
         }
+#if KS_PF_EARLY
+        if (fresh) {
+            load_seg_tables(piv_pool, lut_pool, g, S.P);
+            cached = s;
+        }
+#endif
         __syncthreads();
         const double *in = src + base + threadIdx.x;
         int i0 = 0;
