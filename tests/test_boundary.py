@@ -51,6 +51,21 @@ def test_host_only_entry_points(lib):
     assert lib.ks_workspace_bytes(-1, 1, 0) == 0
 
 
+def test_host_entry_argument_checks(lib):
+    # ks_sort_f64_host validates before any CUDA call: bad sizes / null buffers -> KS_BAD_ARG,
+    # an empty array -> KS_OK, and the status block carries the code
+    import ctypes
+    from paper_1107_3622_b200 import _lib
+    _lib.load()   # sets argtypes
+    st = _lib.KsStatus()
+    assert lib.ks_sort_f64_host(None, -1, None, None, 0, None, 0, ctypes.byref(st)) == _lib.KS_BAD_ARG
+    assert st.code == _lib.KS_BAD_ARG
+    h = (ctypes.c_double * 4)(3.0, 1.0, 2.0, 0.5)
+    assert lib.ks_sort_f64_host(ctypes.addressof(h), 4, None, None, 0, None, 0, ctypes.byref(st)) == _lib.KS_BAD_ARG
+    assert list(h) == [3.0, 1.0, 2.0, 0.5]   # untouched
+    assert lib.ks_sort_f64_host(None, 0, None, None, 0, None, 0, ctypes.byref(st)) == _lib.KS_OK
+
+
 def test_status_struct_layout(tmp_path):
     # the ctypes mirror must match the C compiler's layout of ks_status_t
     import subprocess
