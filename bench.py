@@ -14,9 +14,14 @@ Per step: the input is restored from a pristine device copy and L2 is flushed
 ranks time.  ``e2e`` = the same metric through ``k_sort`` on a pinned HOST
 tensor (H2D + sort + D2H inside the events).
 
---impl reference: the reference's K-sort algorithm on the host CPU (the C
-restatement in oracle/, "port": the reference itself is pure Python and does
-not exist on the GPU box), one full 10M-key array per host thread per step.
+Also on rank 0 at N=1: ``configs`` (C0..C5 device times, bytewise-checked),
+``e2e_list`` (the reference's list[float] KeyArray through k_sort), and
+``cpu_baseline`` = the C restatement of the reference K-sort / heap sort on one
+host core plus the UNMODIFIED Python reference (baseline/_ref) at 1e5 / 1e6.
+
+--impl reference: the reference's K-sort algorithm on all host cores (the C
+restatement in oracle/, "port": the reference is pure Python, so there is no
+native reference build), one full 10M-key array per host thread per step.
 """
 from __future__ import annotations
 
@@ -50,6 +55,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-vendor", action="store_true", help="skip the torch.sort context timing")
+    p.add_argument("--no-configs", action="store_true", help="skip the per-config (C0..C5) timings")
+    p.add_argument("--no-python-ref", action="store_true", help="skip the reference's Python sorters in cpu_baseline")
     return p.parse_args()
 
 
@@ -220,7 +227,7 @@ def run_reference(args):
 # our arm
 # ---------------------------------------------------------------------------
 
-def cpu_baseline(n: int, kind: str):
+def cpu_baseline(n: int, kind: str, with_python: bool = True):
     """The reference algorithm (C restatement, 1 thread) on a bounded sample."""
     import numpy as np
     from oracle import oracle as O
@@ -240,11 +247,95 @@ def cpu_baseline(n: int, kind: str):
         model = [ln.split(":", 1)[1].strip() for ln in open("/proc/cpuinfo") if ln.startswith("model name")][0]
     except Exception:
         model = "unknown"
-    return {"value": n / statistics.mean(kt), "unit": "keys/s", "cores": 1, "kind": "port",
-            "sample": f"{reps} x full {n:,}-key array, K-sort (C restatement of sort_core.k_sort, 1 thread); "
-                      f"heap sort 1 x {n:,}",
-            "ksort_s": statistics.mean(kt), "heapsort_s": ht, "heapsort_value": n / ht,
-            "host_cpu": model, "host_cpus": os.cpu_count()}
+    out = {"value": n / statistics.mean(kt), "unit": "keys/s", "cores": 1, "kind": "port",
+           "sample": f"{reps} x full {n:,}-key array, K-sort (C restatement of sort_core.k_sort, 1 thread); "
+                     f"heap sort 1 x {n:,}",
+           "ksort_s": statistics.mean(kt), "heapsort_s": ht, "heapsort_value": n / ht,
+           "host_cpu": model, "host_cpus": os.cpu_count()}
+    if with_python:
+        out["python_reference"] = python_reference_baseline()
+    return out
+
+
+def python_reference_baseline():
+    """The UNMODIFIED reference (baseline/_ref, Python) k_sort and heap_sort on
+    the reference's own list[float] inputs, timed like its harness
+    (perf_counter_ns around the call only, bench.py:148-152 of the reference);
+    1 core (the reference is single-threaded).  Bounded sample: n = 1e5 (3
+    reps) and 1e6 (1 rep), ~25 s of CPU work; extrapolations to 1e7 assume
+    n log2 n scaling from the 1e6 sample."""
+    try:
+        from baseline import ref_import
+        sortlab = ref_import.import_sortlab()
+    except Exception as e:   # reference not shipped with the snapshot
+        return {"unavailable": f"{type(e).__name__}: {e}"}
+    import math
+    sc, wl = sortlab.sort_core, sortlab.workload
+    res = {"impl": "sortlab.sort_core.k_sort / heap_sort (unmodified, CPython)", "cores": 1}
+    for n, reps in ((100_000, 3), (1_000_000, 1)):
+        for name, fn in (("ksort", sc.k_sort), ("heapsort", sc.heap_sort)):
+            ts = []
+            for r in range(reps):
+                data = wl.generate(wl.WorkloadSpec(n=n, seed=wl.derive_seed(SEED, r, 0)))
+                t0 = time.perf_counter_ns()
+                fn(data)
+                ts.append((time.perf_counter_ns() - t0) / 1e9)
+                assert sc.is_sorted(data)
+            res[f"{name}_{n}_s"] = statistics.mean(ts)
+            res[f"{name}_{n}_keys_per_s"] = n / statistics.mean(ts)
+    scale = (1e7 * math.log2(1e7)) / (1e6 * math.log2(1e6))
+    res["ksort_1e7_s_extrapolated"] = res["ksort_1000000_s"] * scale
+    res["heapsort_1e7_s_extrapolated"] = res["heapsort_1000000_s"] * scale
+    res["sample"] = "n=1e5 x3 and n=1e6 x1 per sorter, reference generator, derive_seed(20260816, r, 0)"
+    return res
+
+
+def time_configs(K, torch, flush, stream, reps: int = 10):
+    """Every BASELINE.json config (C0..C5) on this GPU: median of `reps` sorts
+    after 3 warm-ups, input restored and L2 flushed outside the CUDA events,
+    output checked bytewise against torch.sort of the same input."""
+    out = {}
+
+    def timeit(fn, prep):
+        ts = []
+        for r in range(reps + 3):
+            prep()
+            flush.zero_()
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            if r >= 3:
+                ts.append(a.elapsed_time(b))
+        return statistics.median(ts), min(ts)
+
+    for name, n, kind in (("C1", 100_000, "uniform01"), ("C2", 1_000_000, "uniform01"),
+                          ("C3", 7_000_000, "uniform01"), ("C0", 10_000_000, "uniform01"),
+                          ("C5", 10_000_000, "dup256")):
+        p = K.generate_device(n, SEED, kind)
+        k = torch.empty_like(p)
+        ms, mn = timeit(lambda: K.k_sort(k), lambda: k.copy_(p))
+        ok = bool(torch.equal(k.view(torch.int64), torch.sort(p).values.view(torch.int64)))
+        st = K.last_stats
+        out[name] = {"n": n, "kind": kind, "ms": ms, "ms_min": mn, "keys_per_s": n / (ms * 1e-3), "correct": ok,
+                     "bytes_per_key": st.bytes_moved / n,
+                     "roofline_frac": st.bytes_moved / (ms * 1e-3) / 1e9 / peaks()[0]}
+    # C4: 500 x 100K independent arrays, per-array seeds derive_seed(seed, r, 0), one segmented call
+    from oracle import oracle as O   # seed derivation only (pure arithmetic)
+    seg, nseg = 100_000, 500
+    p = torch.cat([K.generate_device(seg, O.derive_seed(SEED, r, 0)) for r in range(nseg)])
+    off = torch.arange(0, (nseg + 1) * seg, seg, dtype=torch.int64, device="cuda")
+    k = torch.empty_like(p)
+    ms, mn = timeit(lambda: K.k_sort_segments(k, off), lambda: k.copy_(p))
+    want = torch.sort(p.view(nseg, seg), dim=1).values.reshape(-1)
+    ok = bool(torch.equal(k.view(torch.int64), want.view(torch.int64)))
+    st = K.last_stats
+    out["C4"] = {"n": nseg * seg, "kind": f"{nseg} x {seg:,} uniform01 (k_sort_segments)", "ms": ms, "ms_min": mn,
+                 "keys_per_s": nseg * seg / (ms * 1e-3), "correct": ok, "bytes_per_key": st.bytes_moved / (nseg * seg),
+                 "roofline_frac": st.bytes_moved / (ms * 1e-3) / 1e9 / peaks()[0]}
+    return out
 
 
 def run_ours(args):
@@ -297,9 +388,11 @@ def run_ours(args):
     my_ms = sum(step_ms)
     max_ms = max_over_ranks(my_ms, world, "cuda")
     stats = K.last_stats
-    # correctness of the last timed output: sorted and a permutation (checksum of bits)
-    ok = bool(K.is_sorted(keys))
-    ok = ok and int(keys.view(torch.int64).sum().item()) == int(pristine.view(torch.int64).sum().item())
+    # correctness of the last timed output: bytewise equal to the sorted input
+    # (the workloads hold no -0.0, so every correct sort has the reference's bytes)
+    want = torch.sort(pristine).values
+    ok = bool(torch.equal(keys.view(torch.int64), want.view(torch.int64)))
+    del want
 
     # one profiled sort (per-phase CUDA events on the launching stream)
     prep()
@@ -349,11 +442,35 @@ def run_ours(args):
         e2e = {"value": world * n / (statistics.mean(e2e_ms) * 1e-3), "unit": "keys/s",
                "h2d_bytes_per_step": 8 * n, "d2h_bytes_per_step": 8 * n, "ms_per_step": statistics.mean(e2e_ms)}
 
+    # end to end through the reference's own KeyArray: a list[float] in, sorted in place
+    e2e_list = None
+    if not args.no_e2e and world == 1:
+        lst_pristine = pristine.cpu().tolist()
+        t_list = []
+        for i in range(3):
+            lst = list(lst_pristine)
+            t0 = time.perf_counter()
+            K.k_sort(lst)
+            t_list.append(time.perf_counter() - t0)
+        ok_list = lst == sorted(lst_pristine)
+        del lst, lst_pristine
+        e2e_list = {"value": n / statistics.median(t_list[1:]), "unit": "keys/s",
+                    "ms_per_step": 1e3 * statistics.median(t_list[1:]), "h2d_bytes_per_step": 8 * n,
+                    "d2h_bytes_per_step": 8 * n, "correct": ok_list,
+                    "timing": "host perf_counter around k_sort(list) (bench.py:149-151 convention): list -> "
+                              "packed float64 -> H2D -> sort -> D2H -> list rewritten in place"}
+
+    configs = None
+    if world == 1 and not args.no_configs:
+        configs = time_configs(K, torch, flush, stream)
+
     if rank != 0:
         return
     value = job_value(world, n, args.steps, max_ms)
     ms_per_step = max_ms / args.steps
     multi_pass_gbs = stats.bytes_moved / (ms_per_step * 1e-3) / 1e9
+    s8d_bytes = 16 * (stats.keys_partitioned + stats.keys_leaf_sorted)   # SURVEY 8(d) accounting
+    dom_bytes = phase[dom]["bytes"] / max(1, phase[dom]["launches"])
     line = {
         "metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -365,34 +482,50 @@ def run_ours(args):
                    "vs_baseline_ref": "paper Table 1 K-sort 10M = 8.2293 s (PAPER.md:95)"},
         "gpu_launches": launches,
         "correct": ok,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_gbs, "peak": hbm, "unit": "GB/s",
-                     "frac": dom_gbs / hbm, "traffic": ncu_traffic(dom, n, args.kind), "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": phase[dom]["bytes"] / max(1, phase[dom]["launches"])},
+        # the north star's roofline: all bytes the engine's passes read and write
+        # (device-side tally of this run: count reads, scatter read+write, local
+        # partitions, on-chip leaf read+write) over the step time, vs the measured
+        # HBM copy peak; plus the ideal single read+write pass
+        "roofline": {"bound": "hbm", "scope": "whole sort, all passes (engine's own bytes)",
+                     "achieved": multi_pass_gbs, "peak": hbm, "unit": "GB/s", "frac": multi_pass_gbs / hbm,
+                     "traffic": ncu_traffic("sort", n, args.kind), "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_sort": stats.bytes_moved, "bytes_per_key": stats.bytes_moved / n,
+                     "frac_survey_8d": (s8d_bytes / (ms_per_step * 1e-3) / 1e9) / hbm,
+                     "survey_8d_bytes_per_sort": s8d_bytes,
+                     "ideal_single_pass_frac": (16 * n / (ms_per_step * 1e-3) / 1e9) / hbm,
+                     "frac_of_8tbs": multi_pass_gbs / 8000.0,
+                     "dominant_kernel": {"kernel": dom, "achieved": dom_gbs, "peak": hbm, "unit": "GB/s",
+                                         "frac": dom_gbs / hbm, "algorithmic_bytes_per_launch": dom_bytes,
+                                         "traffic": ncu_traffic(dom, n, args.kind),
+                                         "timing": "CUDA events of one KS_FLAG_PROFILE sort"}},
         "multi_pass": {"bytes_per_sort": stats.bytes_moved, "bytes_per_key": stats.bytes_moved / n,
                        "achieved_gbs": multi_pass_gbs, "frac_of_measured": multi_pass_gbs / hbm,
                        "frac_of_8tbs": multi_pass_gbs / 8000.0, "levels": stats.levels,
-                       "leaves": stats.leaves, "keys_leaf_sorted": stats.keys_leaf_sorted,
+                       "leaves": stats.leaves, "keys_partitioned": stats.keys_partitioned,
+                       "keys_leaf_sorted": stats.keys_leaf_sorted,
                        "ideal_single_pass_frac": (16 * n / (ms_per_step * 1e-3) / 1e9) / hbm},
-        # the north star's multi-pass roofline: the traffic of K-sort's own partition
-        # passes (~16.5 passes x 16 B = 264 B/key with on-chip
-        # leaves of <= 8192 keys; the full reference tree: 30.4 x 16 B = 486 B/key)
-        # at peak HBM bandwidth, against this step time (frac > 1: faster than
-        # streaming K-sort's passes at peak)
-        "ksort_multi_pass_roofline": {
-            "bytes_per_key": KSORT_PASS_BYTES_PER_KEY, "peak_gbs": hbm,
-            "floor_ms": KSORT_PASS_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3,
-            "frac": (KSORT_PASS_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3) / ms_per_step,
-            "full_tree_bytes_per_key": KSORT_TREE_BYTES_PER_KEY,
-            "full_tree_frac": (KSORT_TREE_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3) / ms_per_step,
-            "source": "SURVEY.md 8(d) and Appendix C (uniform U[0,1) inputs)"},
+        "context": {
+            # a VIRTUAL model, not this engine's bytes: a binary K-sort pipeline that
+            # streams every level of the reference tree down to 8192-key on-chip
+            # leaves (~16.5 passes x 16 B = 264 B/key) at peak
+            # bandwidth, against this step time
+            "virtual_binary_pass_model": {
+                "bytes_per_key": KSORT_PASS_BYTES_PER_KEY, "peak_gbs": hbm,
+                "floor_ms": KSORT_PASS_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3,
+                "ratio_floor_to_step": (KSORT_PASS_BYTES_PER_KEY * n / (hbm * 1e9) * 1e3) / ms_per_step,
+                "full_tree_bytes_per_key": KSORT_TREE_BYTES_PER_KEY,
+                "source": "SURVEY.md 8(d) and Appendix C (uniform U[0,1) inputs)"}},
         "phases": phase,
         "step_ms": step_ms,
         "clocks": clk.summary(),
         "e2e": e2e,
+        "e2e_list": e2e_list,
         "vendor_context": vendor,
     }
+    if configs is not None:
+        line["configs"] = configs
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = cpu_baseline(n, args.kind)
+        line["cpu_baseline"] = cpu_baseline(n, args.kind, with_python=not args.no_python_ref)
     print(json.dumps(line), flush=True)
 
 

@@ -78,15 +78,19 @@ int ks_sort_f64(double *d_keys, int64_t n, void *d_ws, size_t ws_bytes, void *st
  * there and copied back into h_keys, all on `stream` with one synchronisation
  * (the copy back is queued behind the sort before the status is read, so the
  * device never waits for the host between the three steps).  Pinned h_keys
- * gives asynchronous copies.  On any error h_keys keeps its bytes.  Same
- * flags, codes and status as ks_sort_f64. */
+ * gives asynchronous copies.  On KS_NONFINITE, KS_NEED_EXACT, KS_BAD_ARG and
+ * KS_WORKSPACE_SMALL h_keys keeps its bytes (nothing was written to the device
+ * copy); after KS_CUDA_ERROR its contents are undefined.  Same flags, codes and
+ * status as ks_sort_f64. */
 int ks_sort_f64_host(double *h_keys, int64_t n, double *d_keys, void *d_ws, size_t ws_bytes, void *stream,
                      uint32_t flags, ks_status_t *h_status);
 
 /* Batch entry (new API; the reference bench calls k_sort once per array,
  * bench.py:169-173): sort each segment d_keys[off[s]..off[s+1]) independently,
  * exactly as k_sort would sort it.  d_offsets: device int64[n_segments+1],
- * non-decreasing, off[0] >= 0. */
+ * non-decreasing, off[0] >= 0, off[n_segments] <= n_total; the offsets are
+ * validated on the device before any write and violations return KS_BAD_ARG
+ * with d_keys untouched. */
 int ks_sort_f64_segmented(double *d_keys, const int64_t *d_offsets, int64_t n_segments,
                           int64_t n_total, void *d_ws, size_t ws_bytes, void *stream,
                           uint32_t flags, ks_status_t *h_status);

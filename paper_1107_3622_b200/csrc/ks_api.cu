@@ -176,6 +176,7 @@ int ks_sort_f64_segmented(double *d_keys, const int64_t *d_offsets, int64_t n_se
         int rc = fast_sort(d_keys, n_total, reinterpret_cast<const long long *>(d_offsets), n_segments, d_ws,
                            ws_bytes, st, (flags & KS_FLAG_PROFILE) != 0, &r);
         if (rc != KS_OK) return s->code = rc;
+        if (r.bad_arg) return s->code = KS_BAD_ARG;   // offsets outside [0, n_total] or decreasing
         if (r.bad_index >= 0) {
             fill_bad(s, d_keys, r.bad_index, st);
             return s->code;

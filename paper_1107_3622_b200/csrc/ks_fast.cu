@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cstdio>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -317,12 +318,27 @@ __global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
     route_initial(0, n, Lst, st);
 }
 
-__global__ void k_init_segmented(const long long *off, long long nseg0, InitLists Lst, DevStatus *st)
+// Offsets are validated here, before anything is written: a segment with
+// off[s] < 0, off[s+1] < off[s] or off[s+1] > n_total raises bad_arg, which
+// every writing kernel honours (abort_requested) and the call returns
+// KS_BAD_ARG.  Per-pair checks suffice: consecutive pairs share their ends,
+// so valid pairs are disjoint ranges inside the buffer.
+__device__ __forceinline__ bool seg_ok(long long a, long long b, long long n_total)
+{
+    return 0 <= a && a <= b && b <= n_total;
+}
+
+__global__ void k_init_segmented(const long long *off, long long nseg0, long long n_total, InitLists Lst,
+                                 DevStatus *st)
 {
     KS_PDL_ENTRY();
     for (long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x; s < nseg0;
          s += (long long)gridDim.x * blockDim.x) {
         const long long a = off[s], b = off[s + 1];
+        if (!seg_ok(a, b, n_total)) {
+            atomicOr(reinterpret_cast<unsigned *>(&st->bad_arg), 1u);
+            continue;
+        }
         route_initial(a, b - a, Lst, st);
     }
 }
@@ -345,7 +361,7 @@ __device__ __forceinline__ void gate_flush(long long bad, unsigned pz, unsigned 
 // Finiteness gate (sort_core.py:50-59) for keys not covered by the level-0
 // count pass: segments of <= kInitLocalMax keys (they never see a global pass).
 __global__ void k_gate_segments(const double *keys, const long long *off, long long nseg0, long long n_single,
-                                DevStatus *st)
+                                long long n_total, DevStatus *st)
 {
     KS_PDL_ENTRY();
     long long bad = LLONG_MAX;
@@ -360,6 +376,7 @@ __global__ void k_gate_segments(const double *keys, const long long *off, long l
     } else {
         for (long long s = blockIdx.x; s < nseg0; s += gridDim.x) {
             long long a = off[s], b = off[s + 1];
+            if (!seg_ok(a, b, n_total)) continue;  // (flagged by k_init_segmented)
             if (b - a > kInitLocalMax) continue;  // covered by the level-0 count pass
             for (long long i = a + threadIdx.x; i < b; i += blockDim.x) {
                 gate_one(keys[i], i, bad, pz, nz);
@@ -2448,6 +2465,7 @@ static int sm_count()
         cudaError_t e_ = (x);                                                             \
         if (e_ != cudaSuccess) {                                                          \
             fprintf(stderr, "ksort: %s failed: %s\n", #x, cudaGetErrorString(e_));        \
+            cudaGetLastError(); /* a non-sticky error must not fail the next call */      \
             return KS_CUDA_ERROR;                                                         \
         }                                                                                 \
     } while (0)
@@ -2658,10 +2676,13 @@ struct GraphKey {
                ws_bytes == o.ws_bytes;
     }
 };
+// The executable graph is reference-counted: a thread that evicts an entry
+// never destroys a graph another thread has just looked up and is launching.
+using GraphExecPtr = std::shared_ptr<CUgraphExec_st>;
 struct GraphEntry {
     GraphKey key;
     int dev;
-    cudaGraphExec_t exec;
+    GraphExecPtr exec;
     int level, gcur, leaves_run, epoch, launches;
     unsigned long long last_use;
 };
@@ -2707,7 +2728,6 @@ static void graph_store(GraphEntry e)
         size_t victim = 0;
         for (size_t i = 1; i < g_graphs.size(); ++i)
             if (g_graphs[i].last_use < g_graphs[victim].last_use) victim = i;
-        cudaGraphExecDestroy(g_graphs[victim].exec);
         g_graphs.erase(g_graphs.begin() + victim);
     }
     g_graphs.push_back(e);
@@ -2755,16 +2775,21 @@ static const ForkRes *fork_res()
     return &r;
 }
 
+// Capture stream of the calling thread on the current device (thread-local like
+// fork_res: two threads capturing their graphs at once never share a stream).
+struct CaptureStream {
+    cudaStream_t s = nullptr;
+};
 static cudaStream_t capture_stream()
 {
-    static std::mutex mu;
-    static cudaStream_t streams[64] = {};
+    static thread_local CaptureStream cs[64];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
-    if (streams[dev] == nullptr && cudaStreamCreateWithFlags(&streams[dev], cudaStreamNonBlocking) != cudaSuccess)
-        return nullptr;
-    return streams[dev];
+    if (cs[dev].s == nullptr && cudaStreamCreateWithFlags(&cs[dev].s, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        cs[dev].s = nullptr;
+    }
+    return cs[dev].s;
 }
 
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
@@ -2809,7 +2834,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         if (hp) h = *hp;
         return h.overflow ? KS_CUDA_ERROR : KS_OK;
     };
-    auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero); };
+    auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero) || h.bad_arg; };
 
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
     // level 0 of one array: its first P keys ranked into `sorted` (scratch in the
@@ -2851,10 +2876,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             } else
                 K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
             if (n <= kInitLocalMax)
-                K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, st); });
+                K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, n, st); });
         } else {
-            K.run(kPhGate, [&] { launch(k_init_segmented, dim3(sms), dim3(256), 0, stream, d_off, nseg0, Lst, st); });
-            K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 4), dim3(256), 0, stream, keys, d_off, nseg0, 0, st); });
+            K.run(kPhGate, [&] { launch(k_init_segmented, dim3(sms), dim3(256), 0, stream, d_off, nseg0, n, Lst, st); });
+            K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 4), dim3(256), 0, stream, keys, d_off, nseg0, 0, n, st); });
         }
     };
 
@@ -3032,10 +3057,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             stream = user_stream;
             if (ce != cudaSuccess) {
                 fprintf(stderr, "ksort: graph capture failed: %s\n", cudaGetErrorString(ce));
+                cudaGetLastError();
                 return KS_CUDA_ERROR;
             }
-            KS_CK(cudaGraphInstantiate(&e.exec, g, 0));
+            cudaGraphExec_t ge = nullptr;
+            const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
             cudaGraphDestroy(g);
+            KS_CK(ie);
+            e.exec = GraphExecPtr(ge, [](cudaGraphExec_t x) { cudaGraphExecDestroy(x); });
             e.level = level;
             e.gcur = gcur;
             e.leaves_run = leaves_run;
@@ -3045,7 +3074,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             have = true;
         }
         if (have) {
-            KS_CK(cudaGraphLaunch(e.exec, stream));
+            KS_CK(cudaGraphLaunch(e.exec.get(), stream));
             level = e.level;
             gcur = e.gcur;
             leaves_run = e.leaves_run;
@@ -3076,6 +3105,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     res->levels = level + leaves_run;
     res->bad_index = h.bad_index == kNoIndex ? -1 : (long long)h.bad_index;
     res->mixed_zero = (h.pos_zero && h.neg_zero) ? 1 : 0;
+    res->bad_arg = h.bad_arg ? 1 : 0;
     res->bytes_moved = h.bytes_moved;
     res->keys_partitioned = h.keys_partitioned;
     res->keys_leaf = h.keys_leaf;

@@ -19,6 +19,7 @@ struct FastResult {
     int levels;
     long long bad_index;      // -1 if all finite
     int mixed_zero;           // both signed zeros present: rerun in exact mode
+    int bad_arg;              // segmented call: invalid offsets (nothing written)
     unsigned long long bytes_moved, keys_partitioned, keys_leaf;
     long long leaves;
     int launches;

@@ -132,7 +132,7 @@ struct DevStatus {
     long long mat_total;              // count-matrix entries of the current level
     int overflow;                     // a capacity bound was exceeded (bug guard)
     int no_item_pf;                   // small call: the sorters' per-item L2 prefetches are skipped
-    int pad_;
+    int bad_arg;                      // segmented call: an offset pair outside [0, n_total] or decreasing
     int scan_next;                    // tile counter of the single-pass count-matrix scan
     int chunk;                        // keys per chunk of the current level
     unsigned long long bytes_moved;   // algorithmic bytes, all passes
@@ -183,9 +183,10 @@ __device__ __forceinline__ void add_bytes(DevStatus *st, int phase, unsigned lon
 
 __device__ __forceinline__ bool abort_requested(const DevStatus *st)
 {
-    // Non-finite key (sort_core.py:178) or both signed zeros present (the
-    // fast engine's output is bit-exact only when equal keys are bitwise equal).
-    return st->bad_index != kNoIndex || (st->pos_zero && st->neg_zero);
+    // Non-finite key (sort_core.py:178), both signed zeros present (the fast
+    // engine's output is bit-exact only when equal keys are bitwise equal), or
+    // invalid batch offsets (nothing may be written through them).
+    return st->bad_index != kNoIndex || (st->pos_zero && st->neg_zero) || st->bad_arg;
 }
 
 // Monotone LUT bucket of v: t(v) non-decreasing in v.  (v - lo) and the product

@@ -29,7 +29,10 @@ Engines (all on the GPU; there is no CPU fallback):
 
 from __future__ import annotations
 
+import array
+import contextlib
 import ctypes
+import functools
 import threading
 from dataclasses import dataclass
 from typing import Callable, Optional, Union
@@ -102,6 +105,22 @@ def _stream_ptr() -> int:
     if _raw_stream is not None:
         return _raw_stream(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
+
+
+def _on_input_device(fn):
+    """Run an entry point on the device that holds its CUDA tensor argument.
+
+    The workspace, the stream and every library launch use the *current*
+    device; a tensor on another GPU would otherwise be sorted by kernels of
+    the current one (an illegal address without peer access).
+    """
+    @functools.wraps(fn)
+    def wrapper(a, *args, **kwargs):
+        if isinstance(a, torch.Tensor) and a.is_cuda and a.device.index != torch.cuda.current_device():
+            with torch.cuda.device(a.device):
+                return fn(a, *args, **kwargs)
+        return fn(a, *args, **kwargs)
+    return wrapper
 
 
 _tls = threading.local()
@@ -254,10 +273,31 @@ def _sort_host(h: torch.Tensor, flags: int = 0) -> _lib.KsStatus:
     return st
 
 
+def _list_buffer(a: list) -> Optional[array.array]:
+    """A packed float64 copy of a ``list[float]`` KeyArray (array.array: about
+    3x faster to build than a tensor from the list), or None when empty."""
+    if len(a) == 0:
+        return None
+    return array.array("d", a)
+
+
+def _sort_list(a: list, flags: int) -> Optional[_lib.KsStatus]:
+    """k_sort of the reference's KeyArray: pack, copy in, sort, copy back with
+    one synchronisation (ks_sort_f64_host), then rewrite the list in place.
+    Nothing is written to ``a`` when the sort raises (NonFiniteKeyError)."""
+    buf = _list_buffer(a)
+    if buf is None:
+        return None
+    st = _sort_host(torch.frombuffer(buf, dtype=torch.float64), flags)
+    a[:] = buf.tolist()
+    return st
+
+
 # ---------------------------------------------------------------------------
 # reference API
 # ---------------------------------------------------------------------------
 
+@_on_input_device
 def is_sorted(a: ArrayLike) -> bool:
     """True when a is ascending (non-strict) -- sort_core.py:62-67, on the device."""
     s = _Staged(a)
@@ -272,6 +312,7 @@ def is_sorted(a: ArrayLike) -> bool:
     return bool(r.value)
 
 
+@_on_input_device
 def ksort_partition(a: ArrayLike, left: int, right: int,
                     counts: Optional[OpCounts] = None) -> PartitionOutcome:
     """Partition a[left..right] (inclusive) around key = a[left], in place.
@@ -299,6 +340,7 @@ def ksort_partition(a: ArrayLike, left: int, right: int,
     return PartitionOutcome(pivot_index=int(piv.value), flag_used=bool(flag.value))
 
 
+@_on_input_device
 def k_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     """Sort a ascending, in place (sort_core.py:169-217), on the GPU.
 
@@ -310,17 +352,21 @@ def k_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     if h is not None:   # host tensor / ndarray: copy in, sort, copy back with one synchronisation
         n = h.numel()
         st = _sort_host(h, flags)
+    elif isinstance(a, list):
+        n = len(a)
+        st = _sort_list(a, flags)
     else:
         s = _Staged(a)
         n = s.n
         st = _sort_device(s.dev, flags)
         s.write_back()
-    if counts is not None and n >= 2:
+    if counts is not None and n >= 2 and st is not None:
         counts.comparisons += int(st.comparisons)
         counts.moves += int(st.moves)
         counts.max_pending_ranges = max(counts.max_pending_ranges, int(st.max_pending_ranges))
 
 
+@_on_input_device
 def heap_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     """Sort a ascending, in place, with heap sort's contract (sort_core.py:262-286).
 
@@ -329,6 +375,16 @@ def heap_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     zeros or counts are requested, the reference heap sort runs exactly on the
     device so bytes and tallies match the reference's heap_sort.
     """
+    if counts is None and isinstance(a, list):
+        buf = _list_buffer(a)
+        if buf is None:
+            return
+        v = np.frombuffer(buf, dtype=np.float64)
+        z = np.signbit(v[v == 0])
+        if not (z.any() and not z.all()):   # no mixed signed zeros: the K-sort engine's bytes are heap sort's
+            _sort_host(torch.frombuffer(buf, dtype=torch.float64), 0)
+            a[:] = buf.tolist()
+            return
     s = _Staged(a)
     L = _lib.load()
     exact = counts is not None
@@ -352,6 +408,7 @@ def heap_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
         counts.moves += int(st.moves)
 
 
+@_on_input_device
 def k_sort_segments(keys: torch.Tensor, offsets: torch.Tensor, exact: bool = False) -> None:
     """Sort keys[offsets[s]:offsets[s+1]] independently, in place, in one call.
 
@@ -363,6 +420,8 @@ def k_sort_segments(keys: torch.Tensor, offsets: torch.Tensor, exact: bool = Fal
         raise TypeError("keys must be a contiguous 1-D CUDA float64 tensor")
     if not (offsets.is_cuda and offsets.dtype == torch.int64 and offsets.is_contiguous()):
         raise TypeError("offsets must be a contiguous CUDA int64 tensor")
+    if offsets.device != keys.device:
+        raise ValueError("keys and offsets must be on the same device")
     nseg = offsets.numel() - 1
     if nseg <= 0:
         return
