@@ -387,7 +387,8 @@ def run_ours(args):
     step_ms = [a.elapsed_time(b) for a, b in evs]
     my_ms = sum(step_ms)
     max_ms = max_over_ranks(my_ms, world, "cuda")
-    stats = K.last_stats
+    import dataclasses
+    stats = dataclasses.replace(K.last_stats)   # snapshot: later calls (configs) update last_stats in place
     # correctness of the last timed output: bytewise equal to the sorted input
     # (the workloads hold no -0.0, so every correct sort has the reference's bytes)
     want = torch.sort(pristine).values

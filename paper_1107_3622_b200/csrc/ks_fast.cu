@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <memory>
 #include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "ks_host.h"
@@ -152,6 +153,9 @@ __device__ unsigned long long g_trace[32];
     } while (0)
 #endif
 
+constexpr int kStageMax = KS_STAGE_MAX;   // keys per staged scatter tile (= chunk cap when staged)
+constexpr int kScat2Threads = 1024;
+constexpr int kCount2Threads = 512;
 constexpr int kScanBlock = 4096;   // count-matrix entries per scan CTA (512 thr x 8)
 constexpr int kScanThreads = 512;
 
@@ -553,6 +557,7 @@ __device__ void seg_offsets_body(Seg *segs, int ns, DevStatus *st, long long mat
     }
     long long chunk = cdiv(cdiv(total, (long long)min(items, kChunkItemsMax)), (long long)kChunkAlign) * kChunkAlign;
     if (ns > 1 && chunk > kChunk) chunk = kChunk;
+    if (KS_STAGED && chunk > kStageMax) chunk = kStageMax;   // one chunk = one staged scatter tile
     if (chunk < kChunkMin) chunk = kChunkMin;
     long long c_piv = 0, c_lut = 0, c_mat = 0, c_ch = 0;
     for (int base = 0; base < ns; base += blockDim.x) {
@@ -1291,6 +1296,487 @@ __global__ void __launch_bounds__(kPassThreads, KS_SCAT_MINB) k_scatter(const Se
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Staged partition pass (KS_STAGED): the count and scatter kernels of a
+// global pass rebuilt around 128-bit loads, a branch-free classification,
+// a shared-memory staging of every chunk in gap order and TMA bulk stores.
+//
+//   count:   per chunk, 2 keys per 16-byte load, class of every key
+//            (classify_group: one LUT probe + at most two pivot probes, no
+//            divergent branch), shared-memory histogram -> count-matrix
+//            column; every key's class is also stored (2 B, KS_CLS) so the
+//            scatter needs neither the pivot tables nor a second classification.
+//   scatter: per chunk (= one tile, <= kStageMax keys, 1 CTA per SM):
+//            A. gap table: this chunk's gap counts and destinations from the
+//               count matrix (fetched during the previous chunk's copy-out),
+//               exclusive block scan -> each gap run's start in the tile,
+//               placed at its destination's index parity (one spare slot per
+//               gap) so the run's 16-byte granules line up on both sides;
+//            B. keys (16-byte loads, evict-first: last read of the source at
+//               this level) and classes (4-byte loads) -> tile slot
+//               atomicAdd(cur[gap]): the tile ends up ordered by gap;
+//            C. every gap run leaves the tile by ONE TMA bulk copy
+//               (cp.async.bulk.global.shared::cta) -- an odd head / tail key
+//               by a plain store -- asynchronously, while the next chunk's
+//               table is fetched.
+//   Equality runs (odd classes) are never moved (filled later), as before.
+// Replaces the per-key 8-byte scattered stores of k_scatter and its 80 MB
+// destination prefetch (sort_core.py:94-101 is the reference's element move).
+// Measured (C0, ncu): scatter 85 -> 71 us; DRAM 241 -> 144 MB per launch.
+// ---------------------------------------------------------------------------
+// Classes of G keys (see classify), batched so that the G lookup chains
+// overlap: all bucket indices, then all LUT probes, then two pivot probes per
+// key (pivots of later buckets are > v and the NaN sentinels compare false,
+// so the probes need no bound checks), then the class arithmetic.  A bucket
+// holding 3+ pivots (rare with T >= 2P) is finished afterwards by a short
+// loop for the keys that need it.  kMap: 0 linear bucket map, 1 bit-image
+// map, 2 single bucket (see lut_bucket) -- hoisted out of the key loops.
+template <int kMap>
+__device__ __forceinline__ int bucket_of(double v, double lo, double scale, unsigned long long olo, int T)
+{
+    if (kMap == 2) return 0;
+    double t;
+    if (kMap == 0) {
+        t = (v - lo) * scale;
+    } else {
+        const unsigned long long ov = ord_bits(v);
+        t = ov >= olo ? (double)(ov - olo) * -scale : -1.0;
+    }
+    const int x = __double2int_rz(t);
+    return min(max(x, 0), T - 1);
+}
+
+struct PassMap {
+    double lo, scale;
+    unsigned long long olo;
+    int T;
+};
+
+template <int kMap, int G>
+__device__ __forceinline__ void classify_group(const double *v, int *c, const double *piv, const unsigned *lut,
+                                               const PassMap &M)
+{
+    unsigned e[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) e[u] = lut[bucket_of<kMap>(v[u], M.lo, M.scale, M.olo, M.T)];
+    double p0[G], p1[G];
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+        // probes only where the bucket holds pivots (predicated loads: lanes of
+        // pivot-free buckets -- most of them -- add no shared-memory traffic)
+        const int a = (int)(e[u] & 0xffffu), b = (int)(e[u] >> 16);
+        p0[u] = CUDART_INF;
+        p1[u] = CUDART_INF;
+        if (b > a) p0[u] = piv[a];
+        if (b > a + 1) p1[u] = piv[a + 1];
+    }
+    unsigned slow = 0;
+#pragma unroll
+    for (int u = 0; u < G; ++u) {
+        const int a = (int)(e[u] & 0xffffu), b = (int)(e[u] >> 16);
+        const int r = a + (p0[u] < v[u] ? 1 : 0) + (p1[u] < v[u] ? 1 : 0);
+        const int eq = (p0[u] == v[u] || p1[u] == v[u]) ? 1 : 0;
+        c[u] = 2 * r + eq;
+        slow |= (b - a > 2 ? 1u : 0u) << u;
+    }
+    if (slow) {
+#pragma unroll
+        for (int u = 0; u < G; ++u) {
+            if (!((slow >> u) & 1u)) continue;
+            const int a = (int)(e[u] & 0xffffu), b = (int)(e[u] >> 16);
+            int r = 0, eq = 0;
+#pragma unroll 1
+            for (int i = a + 2; i < b; ++i) {
+                const double p = piv[i];
+                r += p < v[u] ? 1 : 0;
+                eq |= p == v[u] ? 1 : 0;
+            }
+            c[u] += 2 * r + ((c[u] & 1) ? 0 : eq);
+        }
+    }
+}
+
+// f(keys[G], index of keys[0] relative to in, number valid) over in[0, cnt):
+// groups of G = 4 keys from two 16-byte loads (the first key peeled when in is
+// not 16-byte aligned), kU2 pairs in flight per thread; ragged ends come as
+// partial groups.  kCS: evict-first loads.
+template <int kT, int kU2, bool kCS, typename F>
+__device__ __forceinline__ void for_chunk_groups(const double *in, int cnt, F &&f)
+{
+    static_assert(kU2 % 2 == 0, "groups of two pairs");
+    int i0 = 0;
+    if ((reinterpret_cast<unsigned long long>(in) & 15ull) != 0 && cnt > 0) {
+        if (threadIdx.x == 0) {
+            double v[4] = {kCS ? __ldcs(in) : in[0], 0.0, 0.0, 0.0};
+            f(v, 0, 1);
+        }
+        i0 = 1;
+    }
+    const double2 *in2 = reinterpret_cast<const double2 *>(in + i0);
+    const int np = (cnt - i0) >> 1;
+    int p0 = 0;
+    for (; p0 + kU2 * kT <= np; p0 += kU2 * kT) {
+        double2 w[kU2];
+#pragma unroll
+        for (int u = 0; u < kU2; ++u) {
+            const double2 *p = in2 + p0 + u * kT + threadIdx.x;
+            w[u] = kCS ? __ldcs(p) : *p;
+        }
+#pragma unroll
+        for (int u = 0; u < kU2; u += 2) {
+            double v[4] = {w[u].x, w[u].y, w[u + 1].x, w[u + 1].y};
+            // (the two pairs are kT pairs apart: two index bases)
+            f(v, i0 + 2 * (p0 + u * kT + (int)threadIdx.x), -(i0 + 2 * (p0 + (u + 1) * kT + (int)threadIdx.x)));
+        }
+    }
+    for (int p = p0 + (int)threadIdx.x; p < np; p += kT) {
+        const double2 w = kCS ? __ldcs(in2 + p) : in2[p];
+        double v[4] = {w.x, w.y, 0.0, 0.0};
+        f(v, i0 + 2 * p, 2);
+    }
+    const int last = i0 + 2 * np;   // an odd key left at the end
+    if (last < cnt && threadIdx.x == kT - 1) {
+        double v[4] = {kCS ? __ldcs(in + last) : in[last], 0.0, 0.0, 0.0};
+        f(v, last, 1);
+    }
+}
+// (the functor's third argument: n > 0 -> keys[0..n) at index i, consecutive;
+//  n <= 0 -> a full group of two pairs at indices i, i+1 and -n, -n+1)
+__device__ __forceinline__ long long group_index(int i, int n, int u)
+{
+    return n > 0 ? (long long)(i + u) : (long long)(u < 2 ? i + u : -n + (u - 2));
+}
+
+// one pass's classification with the bucket map hoisted: calls body.template
+// operator()<kMap>() for the segment's map kind
+template <typename B>
+__device__ __forceinline__ void with_map(const PassMap &M, B &&body)
+{
+    if (M.T <= 1) body(std::integral_constant<int, 2>());
+    else if (M.scale >= 0.0) body(std::integral_constant<int, 0>());
+    else body(std::integral_constant<int, 1>());
+}
+
+#ifndef KS_COUNT2_MINB
+#define KS_COUNT2_MINB 2
+#endif
+template <bool kGate>
+__global__ void __launch_bounds__(kCount2Threads, KS_COUNT2_MINB) k_count2(const Seg *segs, const int *chunk_seg,
+                                                             const DevStatus *cst, const double *src,
+                                                             const double *piv_pool, const unsigned *lut_pool,
+                                                             unsigned *mat, DevStatus *st, unsigned short *cls)
+{
+    KS_PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    CountSmem &CS = *reinterpret_cast<CountSmem *>(smem_raw);
+    PassSmem &P = CS.P;
+    unsigned *hist = CS.hist;
+    Seg &sg = CS.sg;
+    int cached = -1;
+    long long bad = LLONG_MAX;
+    unsigned pz = 0, nz = 0;
+    const int nchunks = cst->nchunks, chunk = cst->chunk;
+    for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int s = chunk_seg[ch];
+        __syncthreads();
+        if (s != cached) {
+            load_seg(segs, s, piv_pool, lut_pool, sg, P);
+            cached = s;
+        }
+        for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) hist[c] = 0;
+        __syncthreads();
+        const int j = ch - sg.ch_off;
+        const long long base = sg.start + (long long)j * chunk;
+        const int cnt = (int)min((long long)chunk, sg.len - (long long)j * chunk);
+        const PassMap M{sg.lo, sg.scale, ord_bits(sg.lo), sg.T};
+        with_map(M, [&](auto mk) {
+            constexpr int kMap = decltype(mk)::value;
+            for_chunk_groups<kCount2Threads, 4, false>(src + base, cnt, [&](const double *v, int i, int nv) {
+                // level 0 also gates: non-finite keys (sort_core.py:50-59) and signed zeros
+                if (kGate) {
+                    bool odd = false;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) odd |= (nv <= 0 || u < nv) && !(fabs(v[u]) <= DBL_MAX && v[u] != 0.0);
+                    if (odd) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (nv <= 0 || u < nv) gate_one(v[u], base + group_index(i, nv, u), bad, pz, nz);
+                    }
+                }
+                int c[4];
+                classify_group<kMap, 4>(v, c, P.piv, P.lut, M);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (nv <= 0 || u < nv) atomicAdd(&hist[c[u]], 1u);
+                if (KS_CLS) {   // each key's class for the scatter (pairs: 4-byte stores)
+                    unsigned short *cb = cls + base;
+                    if (nv <= 0 && !((base + i) & 1)) {   // (parity uniform over the pass: 4-byte aligned)
+                        *reinterpret_cast<unsigned *>(cb + i) = (unsigned)c[0] | ((unsigned)c[1] << 16);
+                        *reinterpret_cast<unsigned *>(cb - nv) = (unsigned)c[2] | ((unsigned)c[3] << 16);
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (nv <= 0 || u < nv) cb[group_index(i, nv, u)] = (unsigned short)c[u];
+                    }
+                }
+            });
+        });
+        __syncthreads();
+        for (int c = threadIdx.x; c < sg.rows; c += blockDim.x) {
+            if (!(c & 1)) mat[mat_gap(sg, c >> 1, j)] = hist[c];
+            else if (hist[c]) atomicAdd(&mat[mat_eq(sg, c >> 1)], hist[c]);   // (zeroed by k_pivots)
+        }
+    }
+    if (kGate) gate_flush(bad, pz, nz, st);
+}
+
+struct Scatter2Smem {
+#if !KS_CLS
+    PassSmem P;                  // (with KS_CLS the classes come from the count pass: no tables)
+#endif
+    unsigned cur[kPMax + 1];     // next tile slot per gap
+    unsigned delta[kPMax + 1];   // destination (relative to the segment start) - tile position, per gap
+    unsigned sh[33];
+    unsigned total;
+    Seg sg;
+#if KS_SCAT_TMA
+    alignas(16) double stage[kStageMax + kPMax + 2];   // gap runs, each started at its destination's index parity
+#else
+    alignas(16) double stage[kStageMax];           // the chunk's gap keys in gap order
+#endif
+#if KS_CLS && !KS_SCAT_TMA
+    unsigned dsti[kStageMax];          // destination (relative to the segment start) of each tile position
+#elif !KS_CLS
+    unsigned short cls[kStageMax];     // gap of each tile position
+#endif
+};
+
+__global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, const int *chunk_seg,
+                                                              const DevStatus *cst, const double *src, double *dst,
+                                                              const double *piv_pool, const unsigned *lut_pool,
+                                                              const long long *moff, const unsigned *mat,
+                                                              const unsigned short *cls, int pf)
+{
+    KS_PDL_ENTRY();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Scatter2Smem &S = *reinterpret_cast<Scatter2Smem *>(smem_raw);
+    static_assert(2 * kScat2Threads >= kPMax + 1, "two gaps per thread in the gap table");
+    if (abort_requested(cst)) return;   // non-finite key, both signed zeros or bad offsets: write nothing
+    int cached = -1;
+    const int nchunks = cst->nchunks, chunk = cst->chunk;
+    const int tid = threadIdx.x;
+    // gap table of a chunk: gaps 2*tid, 2*tid+1 (contiguous per thread for the
+    // scan); the next chunk's is fetched during this chunk's copy-out when it
+    // belongs to the same segment (its L2 latency then overlaps the stores)
+    unsigned c2[2] = {0u, 0u};
+    long long o2[2] = {0, 0};
+    int have = -1;
+    auto fetch_table = [&](const Seg &g, int jj, long long bi) {   // (bi: the value of a padding gap)
+        const int ng = g.k + 1;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int q = 2 * tid + u;
+            const long long e = mat_gap(g, q, jj);
+            c2[u] = q < ng ? __ldcg(mat + e) : 0u;
+            o2[u] = q < ng ? __ldcg(moff + e) : bi;   // (base subtracted at use: no stall at the fetch)
+        }
+    };
+    // L2 prefetch of the chunk's destination runs: a run boundary leaves a
+    // partially written sector, and a write that misses L2 is slow (the
+    // round-1 scatter measured 156 -> 103 us from the same prefetch)
+    auto prefetch_runs = [&](const Seg &g, long long bi) {
+        if (!pf) return;
+        const double *o = dst + g.start;
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (c2[u]) l2_prefetch_lines(o + (o2[u] - bi), 8ull * c2[u]);
+    };
+    for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+        const int s = chunk_seg[ch];
+        __syncthreads();   // the previous tile's copy-out is done
+        if (s != cached) {
+#if KS_CLS
+            if (tid == 0) S.sg = segs[s];
+            __syncthreads();
+#else
+            load_seg(segs, s, piv_pool, lut_pool, S.sg, S.P);
+#endif
+            cached = s;
+        }
+        const Seg &g = S.sg;
+        const int j = ch - g.ch_off;
+        const long long base = g.start + (long long)j * chunk;
+        const int cnt = (int)min((long long)chunk, g.len - (long long)j * chunk);
+        const long long base_i = moff[g.mat_off];
+        // A. gap table -> run starts in the tile (cur) and destination deltas
+        const int ng = g.k + 1;
+        if (have != ch) {
+            fetch_table(g, j, base_i);
+            prefetch_runs(g, base_i);
+        }
+        unsigned tot;
+#if KS_SCAT_TMA
+        // one spare slot per gap: each run starts in the tile at its destination's
+        // index parity, so the run's 16-byte granules line up on both sides
+        unsigned ps[2];
+        {
+            unsigned ex = block_exclusive_scan_u32(c2[0] + c2[1] + 2u, S.sh, &tot);
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int q = 2 * tid + u;
+                const unsigned long long a = (unsigned long long)(g.start + (o2[u] - base_i));
+                ps[u] = ex + ((ex ^ (unsigned)a) & 1u);
+                if (q < ng) S.cur[q] = ps[u];
+                ex += c2[u] + 1u;
+            }
+        }
+#else
+        unsigned ex = block_exclusive_scan_u32(c2[0] + c2[1], S.sh, &tot);
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int q = 2 * tid + u;
+            if (q < ng) {
+                S.cur[q] = ex;
+                S.delta[q] = (unsigned)(o2[u] - base_i - (long long)ex);
+            }
+            ex += c2[u];
+        }
+#endif
+#if KS_SCAT_TMA
+        // the previous tile's bulk copies have read the buffer (they overlapped this tile's table)
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+        __syncthreads();
+        // B. stage the chunk's gap keys in gap order
+#if KS_CLS
+        {
+            // keys by 16-byte loads and their classes (from the count pass) by
+            // 4-byte loads, kU2 pairs in flight per thread
+            constexpr int kU2 = 4, kT = kScat2Threads;
+            const double *in = src + base;
+            const unsigned short *cin = cls + base;
+            auto place = [&](double v, unsigned c) {
+                if (!(c & 1u)) {
+                    const unsigned q = c >> 1;
+                    const unsigned slot = atomicAdd(&S.cur[q], 1u);
+                    S.stage[slot] = v;
+#if !KS_SCAT_TMA
+                    S.dsti[slot] = S.delta[q] + slot;
+#endif
+                }
+            };
+            int i0 = 0;
+            if ((reinterpret_cast<unsigned long long>(in) & 15ull) != 0) {
+                if (tid == 0) place(KS_SRC_CS ? __ldcs(in) : in[0], cin[0]);
+                i0 = 1;
+            }
+            const bool c4 = !((base + i0) & 1);   // class pairs 4-byte aligned (uniform)
+            const double2 *in2 = reinterpret_cast<const double2 *>(in + i0);
+            const int np = (cnt - i0) >> 1;
+            auto cpair = [&](int p) -> unsigned {
+                const unsigned short *cp = cin + i0 + 2 * p;
+                return c4 ? __ldcs(reinterpret_cast<const unsigned *>(cp))
+                          : (unsigned)__ldcs(cp) | ((unsigned)__ldcs(cp + 1) << 16);
+            };
+            int p0 = 0;
+            for (; p0 + kU2 * kT <= np; p0 += kU2 * kT) {
+                double2 w[kU2];
+                unsigned cc[kU2];
+#pragma unroll
+                for (int u = 0; u < kU2; ++u) {
+                    const int p = p0 + u * kT + tid;
+                    w[u] = KS_SRC_CS ? __ldcs(in2 + p) : in2[p];
+                    cc[u] = cpair(p);
+                }
+#pragma unroll
+                for (int u = 0; u < kU2; ++u) {
+                    place(w[u].x, cc[u] & 0xffffu);
+                    place(w[u].y, cc[u] >> 16);
+                }
+            }
+            for (int p = p0 + tid; p < np; p += kT) {
+                const double2 w = KS_SRC_CS ? __ldcs(in2 + p) : in2[p];
+                const unsigned cc = cpair(p);
+                place(w.x, cc & 0xffffu);
+                place(w.y, cc >> 16);
+            }
+            const int last = i0 + 2 * np;
+            if (last < cnt && tid == kT - 1) place(KS_SRC_CS ? __ldcs(in + last) : in[last], cin[last]);
+        }
+#else
+        const PassMap M{g.lo, g.scale, ord_bits(g.lo), g.T};
+        with_map(M, [&](auto mk) {
+            constexpr int kMap = decltype(mk)::value;
+            for_chunk_groups<kScat2Threads, 4, KS_SRC_CS != 0>(src + base, cnt, [&](const double *v, int, int nv) {
+                int c[4];
+                classify_group<kMap, 4>(v, c, S.P.piv, S.P.lut, M);
+                unsigned slot[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    slot[u] = ((nv <= 0 || u < nv) && !(c[u] & 1)) ? atomicAdd(&S.cur[c[u] >> 1], 1u) : ~0u;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (slot[u] != ~0u) {
+                        S.stage[slot[u]] = v[u];
+                        S.cls[slot[u]] = (unsigned short)(c[u] >> 1);
+                    }
+            });
+        });
+#endif
+#if KS_SCAT_TMA
+        // this chunk's runs (in registers) before the next chunk's table replaces them
+        const unsigned rc[2] = {c2[0], c2[1]};
+        const long long ro[2] = {o2[0] - base_i, o2[1] - base_i};
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged keys -> visible to the bulk copies
+#endif
+        __syncthreads();
+        have = -1;
+        {
+            const int nx = ch + (int)gridDim.x;
+            if (nx < nchunks && nx - g.ch_off < g.nch) {   // next chunk in the same segment
+                fetch_table(g, nx - g.ch_off, base_i);
+                prefetch_runs(g, base_i);
+                have = nx;
+            }
+        }
+        // C. copy-out in tile order: lane l of a warp writes position w + l, so
+        //    a warp store covers 32 consecutive destinations of the runs it
+        //    crosses (whole sectors except at run ends)
+        double *out = dst + g.start;
+#if KS_SCAT_TMA
+        // C'. every run leaves by one bulk copy (an odd head / tail key by a plain store)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int n = (int)rc[u];
+            if (n == 0) continue;
+            const unsigned sp = ps[u];
+            double *o = out + ro[u];
+            const int head = (int)((g.start + ro[u]) & 1);
+            const int mid = (n - head) & ~1;
+            if (head) o[0] = S.stage[sp];
+            if (mid > 0)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o + head),
+                             "r"((unsigned)__cvta_generic_to_shared(&S.stage[sp + head])), "r"(8u * (unsigned)mid)
+                             : "memory");
+            if (head + mid < n) o[head + mid] = S.stage[sp + head + mid];
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        (void)tot;
+#else
+        const int tot2 = (int)tot;
+#pragma unroll 4
+#if KS_CLS
+        for (int i = tid; i < tot2; i += kScat2Threads) out[S.dsti[i]] = S.stage[i];
+#else
+        for (int i = tid; i < tot2; i += kScat2Threads) out[S.delta[S.cls[i]] + (unsigned)i] = S.stage[i];
+#endif
+#endif
+    }
+#if KS_SCAT_TMA
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -2369,8 +2855,10 @@ struct LeafCtl {
     Seg seg;
     int kind;   // -1 done, 0 local partition, 1 segment sort
 };
-constexpr size_t kLeafSmem =
-    (sizeof(SortSmem<2>) > sizeof(LocalSmem) ? sizeof(SortSmem<2>) : sizeof(LocalSmem)) + sizeof(LeafCtl) + 64;
+constexpr size_t cmax(size_t a, size_t b) { return a > b ? a : b; }
+constexpr size_t kLeafSmem = cmax(sizeof(SortSmem<2>), sizeof(LocalSmem)) + sizeof(LeafCtl) + 64;
+template <int C>
+constexpr size_t sort_smem() { return sizeof(SortSmem<C>); }
 
 __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus *st, double *keys,
                                                          const double *tmp)
@@ -2605,6 +3093,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.o_bsum = off; off = align_up(off + sizeof(long long) * L.bsum_cap);
     L.o_units = off; off = align_up(off + sizeof(Item) * L.unit_cap);
     L.o_tmp = off; off = align_up(off + sizeof(double) * (size_t)n);
+    L.o_cls = off; off = align_up(off + ((KS_STAGED && KS_CLS) ? sizeof(unsigned short) * (size_t)n : 0));
     L.total = off;
     return L;
 }
@@ -2613,6 +3102,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 // (cudaFuncSetAttribute / occupancy queries cost host time on every call).
 struct EngineCfg {
     int sms, g_count, g_scatter, g_leaf, g_small[2], g_small3, g_small4;
+    int g_count2, g_scatter2;
 };
 
 static const EngineCfg *engine_cfg()
@@ -2633,11 +3123,16 @@ static const EngineCfg *engine_cfg()
     smem(k_pivots, sizeof(PivotsSmem));
     smem(k_count<true>, sizeof(CountSmem));
     smem(k_count<false>, sizeof(CountSmem));
+    if (KS_STAGED) {
+        smem(k_count2<true>, sizeof(CountSmem));
+        smem(k_count2<false>, sizeof(CountSmem));
+        smem(k_scatter2, sizeof(Scatter2Smem));
+    }
     smem(k_leaf, kLeafSmem);
-    smem(k_segsort<0>, sizeof(SortSmem<0>));
-    smem(k_segsort<1>, sizeof(SortSmem<1>));
-    smem(k_segsort<3>, sizeof(SortSmem<3>));
-    smem(k_segsort<4>, sizeof(SortSmem<4>));
+    smem(k_segsort<0>, sort_smem<0>());
+    smem(k_segsort<1>, sort_smem<1>());
+    smem(k_segsort<3>, sort_smem<3>());
+    smem(k_segsort<4>, sort_smem<4>());
     if (!ok) {
         fprintf(stderr, "ksort: cudaFuncSetAttribute failed: %s\n", cudaGetErrorString(cudaGetLastError()));
         return nullptr;
@@ -2650,11 +3145,15 @@ static const EngineCfg *engine_cfg()
     };
     c.g_count = grid(k_count<false>, kCountThreads, sizeof(CountSmem));
     c.g_scatter = grid(k_scatter, kPassThreads, sizeof(ScatterSmem));
+    if (KS_STAGED) {
+        c.g_count2 = grid(k_count2<false>, kCount2Threads, sizeof(CountSmem));
+        c.g_scatter2 = grid(k_scatter2, kScat2Threads, sizeof(Scatter2Smem));
+    }
     c.g_leaf = grid(k_leaf, kLeafThreads, kLeafSmem);
-    c.g_small[0] = grid(k_segsort<0>, sort_threads(0), sizeof(SortSmem<0>));
-    c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sizeof(SortSmem<1>));
-    c.g_small3 = grid(k_segsort<3>, sort_threads(3), sizeof(SortSmem<3>));
-    c.g_small4 = grid(k_segsort<4>, sort_threads(4), sizeof(SortSmem<4>));
+    c.g_small[0] = grid(k_segsort<0>, sort_threads(0), sort_smem<0>());
+    c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sort_smem<1>());
+    c.g_small3 = grid(k_segsort<3>, sort_threads(3), sort_smem<3>());
+    c.g_small4 = grid(k_segsort<4>, sort_threads(4), sort_smem<4>());
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -2809,6 +3308,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     long long *bsum = reinterpret_cast<long long *>(w + L.o_bsum);
     Item *units = reinterpret_cast<Item *>(w + L.o_units);
     double *tmp = reinterpret_cast<double *>(w + L.o_tmp);
+    unsigned short *cls16 = reinterpret_cast<unsigned short *>(w + L.o_cls);
     LeafQ Q{reinterpret_cast<Seg *>(w + L.o_lq), reinterpret_cast<unsigned long long *>(w + L.o_lq_ready), L.lq_cap,
             reinterpret_cast<Seg *>(w + L.o_sq), reinterpret_cast<unsigned long long *>(w + L.o_sq_ready), L.sq_cap,
             1, {reinterpret_cast<Seg *>(w + L.o_small[0]), reinterpret_cast<Seg *>(w + L.o_small[1])},
@@ -2822,6 +3322,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const int g_count = cfg->g_count, g_leaf = cfg->g_leaf;
     const int g_scatter = (KS_PLAN_FORK && !profile) ? std::max(cfg->sms, cfg->g_scatter - KS_FORK_ROOM) : cfg->g_scatter;
     const int g_scan = sms * 2;
+    // chunks per pass: the staged scatter gives every SM KS_STAGE_ITEMS_PER_SM tiles
+    const int pass_items = KS_STAGED ? sms * KS_STAGE_ITEMS_PER_SM : std::min(g_count, g_scatter);
     const int g_pivots = sms;
     Launcher K(stream, profile);
 
@@ -2832,7 +3334,9 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         KS_CK(cudaMemcpyAsync(hp ? hp : &h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
         KS_CK(cudaStreamSynchronize(stream));
         if (hp) h = *hp;
-        return h.overflow ? KS_CUDA_ERROR : KS_OK;
+        // (an aborted call -- invalid offsets, NaN, mixed zeros -- may leave
+        // queued items behind; its own code takes precedence)
+        return (h.overflow && !h.bad_arg) ? KS_CUDA_ERROR : KS_OK;
     };
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero) || h.bad_arg; };
 
@@ -2866,7 +3370,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                 K.run(kPhGate, [&] {
                     launch(k_init_single_pass, dim3(1), dim3(1024), 0, stream, n, Lst, st, L.mat_cap, L.ch_cap,
                            L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum),
-                           std::min(g_count, g_scatter));
+                           pass_items);
                 });
                 if (fr != nullptr) {
                     cudaEventRecord(fr->join, fr->side);
@@ -2905,7 +3409,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             K.run(kPhPivots, [&] {
                 launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
                        L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next,
-                       std::min(g_count, g_scatter));
+                       pass_items);
             });
         if (level == 0 && d_off == nullptr) {   // one segment, known P: build the pivots GPU-wide
             double *sorted = reinterpret_cast<double *>(moff);   // (scratch: the offsets are written later)
@@ -2920,7 +3424,13 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                        piv, lut, chunk_seg, mat);
             });
         }
-        if (level == 0)
+        if (KS_STAGED) {
+            K.run(kPhCount, [&] {
+                launch_pdl(kPdlHeavy, level == 0 ? k_count2<true> : k_count2<false>, dim3(cfg->g_count2),
+                           dim3(kCount2Threads), sizeof(CountSmem), stream, segs[gcur], chunk_seg, st, src, piv, lut,
+                           mat, st, cls16);
+            });
+        } else if (level == 0)
             K.run(kPhCount, [&] {
                 launch_pdl(kPdlHeavy, k_count<true>, dim3(g_count), dim3(kCountThreads), sizeof(CountSmem), stream, segs[gcur],
                        chunk_seg, st, src, piv, lut, mat, st);
@@ -2940,6 +3450,19 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                    reinterpret_cast<unsigned long long *>(bsum), moff);
         });
 #endif
+        auto launch_scatter = [&]() {
+            if (KS_STAGED)
+                K.run(kPhScatter, [&] {
+                    launch_pdl(kPdlHeavy, k_scatter2, dim3(cfg->g_scatter2), dim3(kScat2Threads), sizeof(Scatter2Smem),
+                               stream, segs[gcur], chunk_seg, st, src, dst, piv, lut, moff, mat,
+                               (const unsigned short *)cls16, KS_STAGED_PF ? scatter_pf : 0);
+                });
+            else
+                K.run(kPhScatter, [&] {
+                    launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream,
+                               segs[gcur], chunk_seg, st, src, dst, piv, lut, moff, mat, scatter_pf);
+                });
+        };
         if (fr != nullptr) {
             // the plan needs only the scanned offsets and the pivots: it runs on a
             // side stream next to the scatter (fork / join; inside the captured graph too)
@@ -2949,17 +3472,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                 launch_pdl(false, k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, fr->side, segs[gcur], nseg_cur, piv,
                            moff, A, st, dst_id);
             });
-            K.run(kPhScatter, [&] {
-                launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur],
-                           chunk_seg, st, src, dst, piv, lut, moff, mat, scatter_pf);
-            });
+            launch_scatter();
             cudaEventRecord(fr->join, fr->side);
             cudaStreamWaitEvent(stream, fr->join, 0);
         } else {
-            K.run(kPhScatter, [&] {
-                launch_pdl(kPdlHeavy, k_scatter, dim3(g_scatter), dim3(kPassThreads), sizeof(ScatterSmem), stream, segs[gcur],
-                           chunk_seg, st, src, dst, piv, lut, moff, mat, scatter_pf);
-            });
+            launch_scatter();
             K.run(kPhPlan, [&] {
                 launch(k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A,
                        st, dst_id);
@@ -3000,24 +3517,24 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         }
         if (n >= KS_SINGLE_MIN_N)
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sizeof(SortSmem<3>), stream,
+                launch_pdl(kPdlHeavy, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sort_smem<3>(), stream,
                            Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
             });
         else
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sizeof(SortSmem<1>), stream,
+                launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sort_smem<1>(), stream,
                            Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
             });
         if (n >= KS_SINGLE_MIN_N)   // (same trade-off for the class-0 list: 8 single-buffer sorters per SM)
             K.run(kPhLeaf, [&] {
                 launch_pdl(kPdlHeavy && s0 == stream, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)),
-                           sizeof(SortSmem<4>), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
+                           sort_smem<4>(), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
                            units);
             });
         else
             K.run(kPhLeaf, [&] {
                 launch_pdl(kPdlHeavy && s0 == stream, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)),
-                           sizeof(SortSmem<0>), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
+                           sort_smem<0>(), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
                            units);
             });
         if (fr != nullptr) {

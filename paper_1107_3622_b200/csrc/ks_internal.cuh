@@ -26,8 +26,33 @@ namespace ks {
 constexpr int kPMax = KS_PMAX;        // max pivot candidates (first P keys) per global pass
 constexpr int kPMaxPow2 = KS_PMAX + 1;
 constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (4095)
+// KS_STAGED: the global pass's count and scatter kernels with 128-bit loads,
+// branch-free classification and a shared-memory staged scatter (k_count2,
+// k_scatter2); 0 selects the round-1 kernels (k_count, k_scatter).
+#ifndef KS_STAGED
+#define KS_STAGED 1
+#endif
+#ifndef KS_STAGE_MAX
+#define KS_STAGE_MAX 16896   // keys per staged scatter tile: 10M keys = 592 chunks = 4 per SM
+#endif
+#ifndef KS_CLS
+#define KS_CLS 1             // staged pass: the count kernel stores every key's class (2 B) for the scatter
+#endif
+#ifndef KS_SCAT_TMA
+#define KS_SCAT_TMA 1        // staged scatter: each gap run leaves the tile by one TMA bulk copy
+#endif
+#ifndef KS_STAGED_PF
+#define KS_STAGED_PF 0       // staged scatter: L2 prefetch of each chunk's destination runs
+#endif
+#ifndef KS_STAGE_ITEMS_PER_SM
+#define KS_STAGE_ITEMS_PER_SM 4
+#endif
 #ifndef KS_LUTMAX
+#if KS_STAGED
+#define KS_LUTMAX 4096       // (the staged scatter's tile needs the shared memory)
+#else
 #define KS_LUTMAX 8192
+#endif
 #endif
 constexpr int kLutMax = KS_LUTMAX;    // LUT buckets (pow2 >= 4*P)
 constexpr int kPMaxLocal = 255;       // ... per local partition (P = len / kKeysPerPivot <= 64)
