@@ -2276,7 +2276,7 @@ struct SortSmem {
     static constexpr int kPB = kBuckets / kT;               // buckets per thread in the scan
     static constexpr int kBigCap = kCap / (kThreadSortMax + 1) + 1;
     double a[kA];          // the segment as loaded (single buffer: unused, or unit scratch)
-    double b[kCap];        // bucket order
+    alignas(16) double b[kCap + 2];   // bucket order, from b[start & 1] (sorted in place; TMA source)
     unsigned cur[kBuckets];
     int big[kBigCap];
     double red[2][32];
@@ -2456,6 +2456,9 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const long long start = g.start;
     const int m = (int)g.len;
+    // bucket-order buffer placed at the segment's global index parity: bb[i] and
+    // out[i] share their 16-byte alignment (the sorted segment leaves by TMA)
+    double *const bb = S.b + (KS_SEG_TMA ? (int)(start & 1) : 0);
     const double *in = (g.src ? tmp : keys) + start;
     double *out = keys + start;
     constexpr int kLU = kT >= 1024 ? 4 : 8;   // loads in flight per thread (one round trip for most segments)
@@ -2580,6 +2583,11 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             __syncthreads();
         }
         KS_TRS(1);   // histogram
+#if KS_SEG_TMA
+        // the previous segment's bulk store has read bb (rewritten by this
+        // segment's scatter, after the scan's barriers): waited as late as possible
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
         {
             const int b0 = tid * Smem::kPB;
             unsigned c[Smem::kPB];
@@ -2605,12 +2613,12 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
         __syncthreads();
         if (Smem::kSingle) {
-            for_keys<kT, kLU>(in, m, [&](int, double x) { S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x; });
+            for_keys<kT, kLU>(in, m, [&](int, double x) { bb[atomicAdd(&S.cur[bmap(x)], 1u)] = x; });
         } else {
 #pragma unroll 1
             for (int i = tid; i < m; i += kT) {
                 const double x = S.a[i];
-                S.b[atomicAdd(&S.cur[bmap(x)], 1u)] = x;
+                bb[atomicAdd(&S.cur[bmap(x)], 1u)] = x;
             }
         }
         __syncthreads();
@@ -2625,7 +2633,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 const int b = S.big[q];
                 const int s0 = b ? (int)S.cur[b - 1] : 0;
                 const int sz = (int)S.cur[b] - s0;
-                if (!warp_sort_bucket(S.b + s0, sz) && lane == 0)   // skewed: back to the first-key partitioner
+                if (!warp_sort_bucket(bb + s0, sz) && lane == 0)   // skewed: back to the first-key partitioner
                     S.hb[atomicAdd(&S.nhb, 1)] = b;
             }
             __syncthreads();
@@ -2636,7 +2644,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         //    written straight to its final place
 #pragma unroll 1
         for (int i = tid; i < m; i += kT) {
-            const double x = S.b[i];
+            const double x = bb[i];
             const int bk = bmap(x);
             const int e = (int)S.cur[bk];
             const int s0 = bk ? (int)S.cur[bk - 1] : 0;
@@ -2645,7 +2653,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 int r = s0;
 #pragma unroll 1
                 for (int j = s0; j < e; ++j) {
-                    const double y = S.b[j];
+                    const double y = bb[j];
                     r += (y < x || (y == x && j < i)) ? 1 : 0;
                 }
                 pos = r;
@@ -2673,12 +2681,13 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                     if (!Smem::kSingle || q < kMidCap) {
                         mid[q] = b;
                     } else {   // list full: the owner sorts it
-                        smem_insertion_sort(S.b + s0, sz);
-                        for (int i = 0; i < sz; ++i) out_store(out + (s0 + i), S.b[s0 + i]);
+                        smem_insertion_sort(bb + s0, sz);
+                        if (!KS_SEG_TMA)
+                            for (int i = 0; i < sz; ++i) out_store(out + (s0 + i), bb[s0 + i]);
                     }
                     continue;
                 }
-                const double *x = S.b + s0;
+                const double *x = bb + s0;
                 double x0 = x[0], x1 = sz > 1 ? x[1] : CUDART_INF, x2 = sz > 2 ? x[2] : CUDART_INF,
                        x3 = sz > 3 ? x[3] : CUDART_INF;
                 cas(x0, x1, true);
@@ -2686,7 +2695,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 cas(x0, x2, true);
                 cas(x1, x3, true);
                 cas(x1, x2, true);
-                double *o = out + s0;
+                double *o = KS_SEG_TMA ? bb + s0 : out + s0;   // (in place: the bulk store writes it)
                 o[0] = x0;
                 if (sz > 1) o[1] = x1;
                 if (sz > 2) o[2] = x2;
@@ -2700,13 +2709,40 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         const int nmid = Smem::kSingle ? min(S.nmid, kMidCap) : S.nmid;
 #if KS_MID_RANK
         static_assert(kThreadSortMax <= 16, "one half-warp lane per key");
+#if KS_SEG_TMA
+        // in place: both half-warps of a warp run the same iterations, every
+        // lane reads before any lane of its warp writes
+#pragma unroll 1
+        for (int q0 = (tid >> 5) * 2; q0 < nmid; q0 += kT / 16) {
+            const int q = q0 + ((tid >> 4) & 1), l = tid & 15;
+            int s0 = 0, sz = 0, r = 0;
+            double v = 0.0;
+            if (q < nmid) {
+                const int b = mid[q];
+                s0 = b ? (int)S.cur[b - 1] : 0;
+                sz = (int)S.cur[b] - s0;
+                if (l < sz) {
+                    const double *x = bb + s0;
+                    v = x[l];
+#pragma unroll 4
+                    for (int j = 0; j < sz; ++j) {
+                        const double y = x[j];
+                        r += (y < v || (y == v && j < l)) ? 1 : 0;
+                    }
+                }
+            }
+            __syncwarp();
+            if (l < sz) bb[s0 + r] = v;
+            __syncwarp();
+        }
+#else
 #pragma unroll 1
         for (int q = tid >> 4; q < nmid; q += kT / 16) {
             const int b = mid[q], l = tid & 15;
             const int s0 = b ? (int)S.cur[b - 1] : 0;
             const int sz = (int)S.cur[b] - s0;
             if (l < sz) {
-                const double *x = S.b + s0;
+                const double *x = bb + s0;
                 const double v = x[l];
                 int r = 0;
 #pragma unroll 4
@@ -2717,27 +2753,52 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 out_store(out + (s0 + r), v);
             }
         }
+#endif
 #else
 #pragma unroll 1
         for (int q = tid; q < nmid; q += kT) {
             const int b = mid[q];
             const int s0 = b ? (int)S.cur[b - 1] : 0;
             const int sz = (int)S.cur[b] - s0;
-            smem_insertion_sort(S.b + s0, sz);
-            for (int i = 0; i < sz; ++i) out_store(out + (s0 + i), S.b[s0 + i]);
+            smem_insertion_sort(bb + s0, sz);
+            for (int i = 0; i < sz; ++i) out_store(out + (s0 + i), bb[s0 + i]);
         }
 #endif
         // 4c. large buckets (sorted by warps above, or handed back): coalesced copy
-        for (int q = wid; q < nbig; q += kWarps) {
+        for (int q = wid; q < nbig && !KS_SEG_TMA; q += kWarps) {
             const int b = S.big[q];
             const int s0 = b ? (int)S.cur[b - 1] : 0;
             const int sz = (int)S.cur[b] - s0;
-            for (int i = lane; i < sz; i += 32) out_store(out + (s0 + i), S.b[s0 + i]);
+            for (int i = lane; i < sz; i += 32) out_store(out + (s0 + i), bb[s0 + i]);
+        }
+#endif
+#if KS_SEG_TMA
+        // 5. the sorted segment (bb) leaves by one TMA bulk copy (an odd head /
+        //    tail key by a plain store); bb is rewritten only by the next
+        //    segment's scatter, after its wait for this copy's reads
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        {
+            const int h = (int)(start & 1), midn = (m - h) & ~1;
+            if (tid == 0 && midn > 0) {
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + h),
+                             "r"((unsigned)__cvta_generic_to_shared(bb + h)), "r"(8u * (unsigned)midn)
+                             : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            if (tid == (kT > 32 ? 32 : 0) && h) out[0] = bb[0];
+            if (tid == kT - 1 && h + midn < m) out[h + midn] = bb[h + midn];
         }
 #endif
         // hand-backs are published only once their keys are in place
         __syncthreads();
         KS_TRS(3);   // big buckets + in-bucket order + write
+#if KS_SEG_TMA
+        if (S.nhb) {   // (rare) hand-backs are published once the bulk store has landed
+            if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            __syncthreads();
+        }
+#endif
         if (tid < S.nhb) {
             const int b = S.hb[tid];
             const int s0 = b ? (int)S.cur[b - 1] : 0;
@@ -2823,6 +2884,9 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         segs_sorted += 1;
         __syncthreads();
     }
+#endif
+#if KS_SEG_TMA
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // (S reused / freed next)
 #endif
     if (threadIdx.x == 0 && segs_sorted) {
         add_bytes(st, kPhLeaf, 16ull * keys_sorted);
@@ -2920,6 +2984,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
             KS_TR(14);
         } else {
             segsort_one<2>(*reinterpret_cast<SortSmem<2> *>(smem_raw), g, Q, st, keys, tmp);
+#if KS_SEG_TMA
+            // the next item may be a local partition, whose tables overlay S.b
+            if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
             keys_sorted += (unsigned long long)g.len;
             segs_sorted += 1;
             KS_TR(15);
@@ -2930,6 +2998,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
             atomicSub(&st->pending, 1);
         }
     }
+#if KS_SEG_TMA
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#endif
     if (threadIdx.x == 0 && segs_sorted) {
         add_bytes(st, kPhLeaf, 16ull * keys_sorted);
         atomicAdd(&st->keys_leaf, keys_sorted);

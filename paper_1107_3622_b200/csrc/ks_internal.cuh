@@ -38,6 +38,9 @@ constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (4095)
 #ifndef KS_CLS
 #define KS_CLS 1             // staged pass: the count kernel stores every key's class (2 B) for the scatter
 #endif
+#ifndef KS_SEG_TMA
+#define KS_SEG_TMA 0         // segment sorters: the sorted segment leaves shared memory by one TMA bulk copy (measured: C0 +2.3%, C3 +5%; off)
+#endif
 #ifndef KS_SCAT_TMA
 #define KS_SCAT_TMA 1        // staged scatter: each gap run leaves the tile by one TMA bulk copy
 #endif
