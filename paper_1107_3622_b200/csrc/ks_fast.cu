@@ -197,6 +197,7 @@ __device__ __forceinline__ Seg load_item(const Seg *q)
     g.bnd = __ldcg(&q->bnd);
     g.lo = __ldcg(&q->lo);
     g.scale = __ldcg(&q->scale);
+    g.stall = __ldcg(&q->stall);
     return g;
 }
 
@@ -422,9 +423,15 @@ __device__ __forceinline__ double merge_pick(const double *s, int g0, int size, 
     return (B[b] < A[a]) ? B[b] : A[a];
 }
 
+// Stride of the pivot sample: 1 (K-sort's first P keys) unless the segment stalled.
+__device__ __forceinline__ long long pivot_stride(int stall, long long len, int P)
+{
+    return (KS_STALL_GUARD && stall && P > 0 && len / P > 1) ? len / P : 1;
+}
+
 template <int N>
 __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, unsigned *lut, PivotScratch<N> &W,
-                             int &k_out, int &T_out, double &lo_out, double &scale_out)
+                             int &k_out, int &T_out, double &lo_out, double &scale_out, long long stride = 1)
 {
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const int NP = next_pow2(P) < 32 ? 32 : next_pow2(P);
@@ -433,7 +440,7 @@ __device__ void build_pivots(const double *seg, int P, int Treq, double *piv, un
     // merge-path passes with one output per thread
     for (int w = wid; w * 32 < NP; w += nw) {
         const int i = w * 32 + lane;
-        double x[1] = {i < P ? __ldcg(seg + i) : CUDART_INF};
+        double x[1] = {i < P ? __ldcg(seg + i * stride) : CUDART_INF};
         warp_bitonic_sort<1>(x);
         W.sp[i] = x[0];
     }
@@ -665,7 +672,10 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *
         int k, T;
         double lo, scale;
         KS_TR_DECL;
-        build_pivots(src + g.start, g.P, g.T, piv, lut, W, k, T, lo, scale);
+        // K-sort's pivots are the segment's first P keys; a stalled segment (its
+        // parent kept almost all keys in one gap: first-key pivots are making no
+        // progress) takes P keys spread across it instead -- same partition rule
+        build_pivots(src + g.start, g.P, g.T, piv, lut, W, k, T, lo, scale, pivot_stride(g.stall, g.len, g.P));
         KS_TR(11);
         for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = piv[i];
         for (int t = threadIdx.x; t < T; t += blockDim.x) lut_pool[g.lut_off + t] = lut[t];
@@ -1899,8 +1909,9 @@ __device__ __forceinline__ double block_inclusive_max_f64(double x, long long *s
 
 __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long ae, long long el, double pv, int dst_id,
                               const EmitArgs &A, DevStatus *st, long long *sh, long long *sbase, int *mg, double blo,
-                              double bhi)
+                              double bhi, long long plen)
 {
+    const int stall = 4 * gl > 3 * plen ? 1 : 0;   // this gap kept > 3/4 of the parent's keys
     int u_gap = 0, s_gap = 0, l_gap = 0, g_gap = 0, t_gap = 0;
     bool merged = false;
 #if KS_MERGE
@@ -1985,17 +1996,22 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
                   with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemSort), A.Q.epoch);
     if (l_gap) {
         const int i = (int)(sbase[1] + pk_get(xpk, kPkL, 11));
-        const Seg c = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal);
+        Seg c = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal);
+        c.stall = stall;
         if (A.in_leaf) q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, i, c, A.Q.epoch);
         else if (i < A.Q.lcap) A.Q.lq[A.Q.lcap - 1 - i] = c; else st->overflow = 7;   // (read after this launch)
     }
     if (lb_gap) {
         const int i = (int)(sbase[4] + pk_get(xpk, kPkLB, 11));
-        if (i < A.Q.lcap) A.Q.lq[i] = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal); else st->overflow = 7;
+        Seg c = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal);
+        c.stall = stall;
+        if (i < A.Q.lcap) A.Q.lq[i] = c; else st->overflow = 7;
     }
     if (g_gap) {
         const long long gi = sbase[2] + pk_get(xpk, kPkG, 11);
-        if (gi < A.gcap) A.gnext[gi] = make_seg(ag, gl, dst_id); else st->overflow = 4;
+        Seg c = make_seg(ag, gl, dst_id);
+        c.stall = stall;
+        if (gi < A.gcap) A.gnext[gi] = c; else st->overflow = 4;
     }
     // keys in fills / units (block totals; segments < 2^31 keys)
     long long tk;
@@ -2062,7 +2078,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
         const double blo = (have && j > 0) ? piv_pool[g.piv_off + j - 1] : -CUDART_INF;
         const double bhi = (have && j < g.k) ? pv : CUDART_INF;
         const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, sh, sbase, s_mg, blo,
-                                     bhi);
+                                     bhi, g.len);
         if (threadIdx.x == 0) {
             // keys of this chunk's classes [2 j0, 2 min(j0 + kPlanThreads, k + 1))
             const int jend = min(j0 + kPlanThreads, g.k + 1);
@@ -2105,7 +2121,7 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
     int k, T;
     double lo, scale;
     KS_TR_DECL;
-    build_pivots(src, P, lut_for(P, kLutMaxLocal), L.piv, L.lut, L.W, k, T, lo, scale);
+    build_pivots(src, P, lut_for(P, kLutMaxLocal), L.piv, L.lut, L.W, k, T, lo, scale, pivot_stride(g.stall, m, P));
     KS_TR(0);
     const int rows = 2 * k + 1;
     for (int c = threadIdx.x; c < rows; c += blockDim.x) L.hist[c] = 0;
@@ -2169,7 +2185,7 @@ __device__ void local_one(LocalSmem &L, const Seg &g, const EmitArgs &A, DevStat
     const double blo = (have && j > 0) ? L.piv[j - 1] : (g.bnd ? g.lo : -CUDART_INF);
     const double bhi = (have && j < k) ? pv : (g.bnd ? g.scale : CUDART_INF);
     const EmitOut o = emit_pairs(have, g.start + ag, gl, g.start + ae, el, pv, dst_id, A, st, L.sh, L.sbase, L.mg, blo,
-                                 bhi);
+                                 bhi, g.len);
     if (threadIdx.x == 0) account_partition(st, g.len, o, true);
     KS_TR(3);
 #ifdef KS_TRACE

@@ -38,6 +38,9 @@ constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (4095)
 #ifndef KS_CLS
 #define KS_CLS 1             // staged pass: the count kernel stores every key's class (2 B) for the scatter
 #endif
+#ifndef KS_STALL_GUARD
+#define KS_STALL_GUARD 1     // stalled segments take pivots sampled across them (see Seg::stall)
+#endif
 #ifndef KS_SEG_TMA
 #define KS_SEG_TMA 0         // segment sorters: the sorted segment leaves shared memory by one TMA bulk copy (measured: C0 +2.3%, C3 +5%; off)
 #endif
@@ -188,6 +191,9 @@ struct Seg {
     int src;           // local rounds: 0 keys / 1 tmp hold the segment
     int bnd;           // leaf items: all keys lie in [lo, scale] (bounds from the parent's pivots)
     double lo, scale;  // LUT transform t = clamp((v - lo) * scale, 0, T-1)
+    int stall;         // the parent partition kept > 3/4 of its keys in this one gap (presorted,
+                       // reversed, organ-pipe ...): pivots are sampled across the segment
+    int spare_[3];
 };
 
 // Work item of the on-chip finishing pass.
