@@ -3027,6 +3027,43 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
 // ---------------------------------------------------------------------------
 // host plumbing
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// self-check build (KS_CHECK): multiset fingerprint (sum and xor of the bit
+// patterns) of the input and of the output, and per-segment sortedness
+// ---------------------------------------------------------------------------
+struct CheckWords {
+    unsigned long long in_sum, in_xor, out_sum, out_xor, unsorted, bad_tile, pad_[2];
+};
+__global__ void k_check_sum(const double *keys, long long n, unsigned long long *sum, unsigned long long *x)
+{
+    unsigned long long s = 0, z = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned long long b = __double_as_longlong(keys[i]);
+        s += b;
+        z ^= b;
+    }
+    atomicAdd(sum, s);
+    atomicXor(x, z);
+}
+__global__ void k_check_sorted(const double *keys, long long n, const long long *off, long long nseg,
+                               unsigned long long *bad)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x + 1; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        if (keys[i - 1] <= keys[i]) continue;
+        bool boundary = false;   // i starts a segment: no order across segments
+        if (off != nullptr) {
+            long long lo = 0, hi = nseg;   // any s with off[s] == i
+            while (lo < hi) {
+                const long long mid = (lo + hi) >> 1;
+                if (off[mid] < i) lo = mid + 1; else hi = mid;
+            }
+            boundary = lo <= nseg && off[lo] == i;
+        }
+        if (!boundary) atomicAdd(bad, 1ull);
+    }
+}
+
 static int sm_count()
 {
     int dev = 0, sms = 148;
@@ -3181,6 +3218,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.o_units = off; off = align_up(off + sizeof(Item) * L.unit_cap);
     L.o_tmp = off; off = align_up(off + sizeof(double) * (size_t)n);
     L.o_cls = off; off = align_up(off + ((KS_STAGED && KS_CLS) ? sizeof(unsigned short) * (size_t)n : 0));
+    L.o_check = off; off = align_up(off + (KS_CHECK ? 64 : 0));
     L.total = off;
     return L;
 }
@@ -3636,7 +3674,12 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         Q = Qn;
         ++leaves_run;
     };
+    CheckWords *cw = reinterpret_cast<CheckWords *>(w + L.o_check);
     auto spec = [&]() {
+        if (KS_CHECK) {
+            cudaMemsetAsync(cw, 0, sizeof(CheckWords), stream);
+            k_check_sum<<<sms * 4, 256, 0, stream>>>(keys, n, &cw->in_sum, &cw->in_xor);
+        }
         init_launch();
         if (n > kInitLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
         leaf();
@@ -3705,6 +3748,19 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     if (more && h_out != nullptr) {
         KS_CK(cudaMemcpyAsync(h_out, keys, 8ull * n, cudaMemcpyDeviceToHost, stream));
         KS_CK(cudaStreamSynchronize(stream));
+    }
+    if (KS_CHECK && !aborted()) {   // self-check: same multiset, sorted per segment
+        k_check_sum<<<sms * 4, 256, 0, stream>>>(keys, n, &cw->out_sum, &cw->out_xor);
+        k_check_sorted<<<sms * 4, 256, 0, stream>>>(keys, n, d_off, nseg0, &cw->unsorted);
+        CheckWords hc{};
+        KS_CK(cudaMemcpyAsync(&hc, cw, sizeof(hc), cudaMemcpyDeviceToHost, stream));
+        KS_CK(cudaStreamSynchronize(stream));
+        if (hc.in_sum != hc.out_sum || hc.in_xor != hc.out_xor || hc.unsorted || hc.bad_tile) {
+            fprintf(stderr, "ksort: self-check failed (n=%lld nseg=%lld): sum %s xor %s unsorted %llu bad_tile %llu\n",
+                    n, nseg0, hc.in_sum == hc.out_sum ? "ok" : "DIFF", hc.in_xor == hc.out_xor ? "ok" : "DIFF",
+                    hc.unsorted, hc.bad_tile);
+            return KS_CUDA_ERROR;
+        }
     }
     res->levels = level + leaves_run;
     res->bad_index = h.bad_index == kNoIndex ? -1 : (long long)h.bad_index;

@@ -38,6 +38,10 @@ constexpr int kRowsMax = 2 * kPMax + 1;  // classes: gaps + equality runs (4095)
 #ifndef KS_CLS
 #define KS_CLS 1             // staged pass: the count kernel stores every key's class (2 B) for the scatter
 #endif
+#ifndef KS_CHECK
+#define KS_CHECK 0           // self-check build: every fast sort verifies its output (sorted per segment,
+                             // same multiset by bit-pattern sum and xor) and the staged tiles' bounds
+#endif
 #ifndef KS_STALL_GUARD
 #define KS_STALL_GUARD 1     // stalled segments take pivots sampled across them (see Seg::stall)
 #endif
