@@ -48,6 +48,41 @@ __device__ unsigned long long g_trace[32];
 #define KS_TR(slot)
 #endif
 
+#ifdef KS_TIMELINE
+// optional per-item timeline (build with -DKS_TIMELINE): one record per leaf item
+// {smid | kernel << 8 | kind << 16, len, t0, t1} (globaltimer ns), read via ks_timeline_read
+constexpr int kTlCap = 1 << 17;
+__device__ unsigned long long g_tl[4 * kTlCap];
+__device__ unsigned g_tl_n;
+__device__ __forceinline__ unsigned long long tl_now()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsigned long long t0)
+{
+    const unsigned long long t1 = tl_now();
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    const unsigned i = atomicAdd(&g_tl_n, 1u);
+    if (i < (unsigned)kTlCap) {
+        g_tl[4 * i] = smid | ((unsigned long long)kernel << 8) | ((unsigned long long)(kind + 1) << 16);
+        g_tl[4 * i + 1] = (unsigned long long)len;
+        g_tl[4 * i + 2] = t0;
+        g_tl[4 * i + 3] = t1;
+    }
+}
+#define KS_TL_T0 const unsigned long long tl_t0_ = tl_now()
+#define KS_TL(kernel, kind, len) \
+    do {                         \
+        if (threadIdx.x == 0) tl_rec(kernel, kind, len, tl_t0_); \
+    } while (0)
+#else
+#define KS_TL_T0
+#define KS_TL(kernel, kind, len)
+#endif
+
 // build-time variants (experiments; defaults are the measured best)
 #ifndef KS_BATCH
 #define KS_BATCH 0        // batched (overlapped) classify in the count / scatter loops: 1 = all U keys at once
@@ -132,6 +167,9 @@ __device__ unsigned long long g_trace[32];
 #endif
 #ifndef KS_MINB1
 #define KS_MINB1 2        // resident CTAs per SM asked for the 512-thread small-segment sorter
+#endif
+#ifndef KS_LEAF_CHAIN
+#define KS_LEAF_CHAIN 1   // the list sorters start (PDL) on the SMs the leaf kernel's CTAs leave
 #endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
@@ -219,7 +257,18 @@ struct LeafQ {
     int epoch;        // leaf launch these items belong to
     Seg *small[2];    // segments of size classes 0 / 1: sorted by their own CTA shapes after the leaf launch
     int small_cap[2];
+    Seg *hb;          // sorter hand-backs: partitioned by the next leaf launch (its local queue)
+    int hb_cap;
 };
+
+// A skewed bucket the on-chip sorter cannot finish goes back to the first-key
+// partitioner in the NEXT leaf launch: no queue item appears during a launch
+// except from a local partition, so CTAs may leave once none is queued or running.
+__device__ __forceinline__ void hb_push(const LeafQ &Q, const Seg &g, DevStatus *st)
+{
+    const int i = atomicAdd(&st->nhb, 1);
+    if (i < Q.hb_cap) Q.hb[i] = g; else st->overflow = 6;
+}
 
 // small segments (<= sort_cap(1) keys) go to the size-class lists
 __device__ __forceinline__ void small_push(const LeafQ &Q, const Seg &g, DevStatus *st)
@@ -278,7 +327,7 @@ __device__ __forceinline__ void q_push1(bool local, const LeafQ &Q, const Seg &g
         small_push(Q, g, st);
         return;
     }
-    atomicAdd(&st->pending, 1);
+    if (local) atomicAdd(&st->pending, 1);
     q_publish(Q.sq, Q.sq_ready, Q.scap, atomicAdd(&st->sq_claim, 1), with_kind(g, local ? kItemLocal : kItemSort),
               Q.epoch);
 }
@@ -635,6 +684,7 @@ __global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, lo
                                    unsigned long long *tstat, int items)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     __shared__ long long sh[33];
     unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
     for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
@@ -647,6 +697,7 @@ __global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, lo
     __syncthreads();
     seg_offsets_body(Lst.gsegs, st->nseg[0], st, mat_cap, ch_cap, piv_cap, lut_cap, mat, moff, tstat, &st->nseg[1],
                      items, sh);
+    KS_TL(20, 8, 0);
 }
 
 struct PivotsSmem {
@@ -702,6 +753,7 @@ constexpr int kRankParts = 8;   // threads per ranked key (a power of two dividi
 __global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const double *in, int P, double *sorted)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     __shared__ double x[kPMax + 1];
     constexpr int kU = (kPMax + 1 + kRankThreads - 1) / kRankThreads;   // all loads in flight at once
     double t[kU];
@@ -731,6 +783,7 @@ __global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const double *in, i
 #pragma unroll
     for (int o = kRankParts / 2; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (i < P && part == 0) sorted[r] = v;   // (NaN keys -- rejected by the gate -- may collide; all in range)
+    KS_TL(21, 8, 0);
 }
 
 constexpr int kLutCtas = 16;
@@ -739,6 +792,7 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
                                                              unsigned *lut_pool, int *chunk_seg, unsigned *mat)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     __shared__ double piv[kPMax + kPivPad];
     __shared__ long long sh[33];
     const Seg g = segs[0];
@@ -790,6 +844,7 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
             segs[0].scale = scale;
         }
     }
+    KS_TL(22, 8, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1013,6 +1068,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *
                                                                 unsigned long long *tstat, long long *moff)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     constexpr unsigned long long kScanAgg = 1ull << 62, kScanPrefix = 2ull << 62, kScanVal = (1ull << 62) - 1;
     __shared__ long long sh[33];
     __shared__ int s_tile;
@@ -1095,6 +1151,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *
         }
         __syncthreads();   // s_tile / s_excl reuse
     }
+    KS_TL(24, 8, 0);
 }
 
 // start of class c inside segment g (relative), c in [0, rows]; rows -> len
@@ -1479,6 +1536,7 @@ __global__ void __launch_bounds__(kCount2Threads, KS_COUNT2_MINB) k_count2(const
                                                              unsigned *mat, DevStatus *st, unsigned short *cls)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CountSmem &CS = *reinterpret_cast<CountSmem *>(smem_raw);
     PassSmem &P = CS.P;
@@ -1540,6 +1598,7 @@ __global__ void __launch_bounds__(kCount2Threads, KS_COUNT2_MINB) k_count2(const
         }
     }
     if (kGate) gate_flush(bad, pz, nz, st);
+    KS_TL(23, 8, 0);
 }
 
 struct Scatter2Smem {
@@ -1570,6 +1629,7 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
                                                               const unsigned short *cls, int pf)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Scatter2Smem &S = *reinterpret_cast<Scatter2Smem *>(smem_raw);
     static_assert(2 * kScat2Threads >= kPMax + 1, "two gaps per thread in the gap table");
@@ -1787,6 +1847,7 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
 #if KS_SCAT_TMA
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #endif
+    KS_TL(26, 8, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -1972,7 +2033,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
         const int tu = (int)pk_get(tpk, kPkU, 16), tl = (int)pk_get(tpk, kPkL, 11);
         const int tg = (int)pk_get(tpk, kPkG, 11), ts = (int)pk_get(tpk, kPkS, 11);
         const int tlb = (int)pk_get(tpk, kPkLB, 11);
-        if (tl + ts + tlb) atomicAdd(&st->pending, tl + ts + tlb);   // before the slots become claimable
+        if (tl + tlb) atomicAdd(&st->pending, tl + tlb);   // before the slots become claimable
         sbase[4] = tlb ? atomicAdd(&st->lqb_claim, tlb) : 0;
         sbase[0] = tu ? atomicAdd(&st->nunits, tu) : 0;
         sbase[1] = tl ? atomicAdd(A.in_leaf ? &st->sq_claim : &st->lq_claim, tl) : 0;
@@ -2050,6 +2111,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
                                                        const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     __shared__ long long sh[33];
     __shared__ long long sbase[5];
     __shared__ int s_mg[kPlanThreads];
@@ -2086,6 +2148,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
             account_partition(st, len, o, false);
         }
     }
+    KS_TL(25, 8, 0);
 }
 
 // ---------------------------------------------------------------------------
@@ -2819,7 +2882,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
             const int b = S.hb[tid];
             const int s0 = b ? (int)S.cur[b - 1] : 0;
             __threadfence();
-            q_push1(true, Q, make_seg(start + s0, (int)S.cur[b] - s0, 0), st);
+            hb_push(Q, make_seg(start + s0, (int)S.cur[b] - s0, 0), st);
         }
     }
 #ifdef KS_TRACE
@@ -2834,13 +2897,29 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 template <int C>
 __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ? KS_MINB3 : (C == 4 ? KS_MINB4 : KS_MINB1)))
     k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp,
-              const Item *units)
+              const Item *units, int chained)
 {
-    KS_PDL_ENTRY();
+    // chained: launched programmatically behind the leaf kernel (or behind the
+    // other list sorter) and started on the SMs its CTAs leave.  The lists are
+    // final once no local partition is queued or running (`pending`, released
+    // by the partitioner after its list entries); the grid ahead must still
+    // complete before this one does (griddepcontrol.wait at the end).
+    if (chained) {
+        asm volatile("griddepcontrol.launch_dependents;" :::);
+        if (threadIdx.x == 0)
+            while (ld_acquire_s32(&st->pending) != 0) __nanosleep(256);
+        __syncthreads();
+    } else {
+        KS_PDL_ENTRY();
+    }
+    KS_TL_T0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SortSmem<C> &S = *reinterpret_cast<SortSmem<C> *>(smem_raw);
     __shared__ int s_item;
-    if (abort_requested(st)) return;
+    if (abort_requested(st)) {
+        if (chained) asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
     const int n = *count;
     unsigned long long keys_sorted = 0, segs_sorted = 0;
     // thread 0 claims one item ahead and pulls its input and output ranges into
@@ -2875,8 +2954,10 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         const Seg g = s_seg[slot];
         SegFeed f{list, n, 0, &s_seg[slot ^ 1], &s_idx[slot ^ 1], keys, tmp, false, pf};
         if (threadIdx.x == 0) f.d = atomicAdd(next, 1);   // (used after the load phase)
+        KS_TL_T0;
         segsort_one<C>(S, g, Q, st, keys, tmp, f);
         f.after_scatter();   // (no-op unless the segment took no scatter path)
+        KS_TL(10 + C, 1, g.len);
         keys_sorted += (unsigned long long)g.len;
         segs_sorted += 1;
     }
@@ -2909,6 +2990,7 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         atomicAdd(&st->keys_leaf, keys_sorted);
         atomicAdd(&st->leaves, segs_sorted);
     }
+    KS_TL(10 + C, 8, keys_sorted);
     if (C == 0 || C == 4) {   // the last kernel of the launch also finishes the warp units and fills
         constexpr int kW = sort_threads(C) / 32;
         static_assert((C != 0 && C != 4) || kW * sidx_size(kUnitMax) <= SortSmem<C>::kA + SortSmem<C>::kCap,
@@ -2918,6 +3000,7 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         const int nu = st->nunits;
         for (int d = blockIdx.x * kW + (threadIdx.x >> 5); d < nu; d += gridDim.x * kW) finish_item(units[d], keys, tmp, sm);
     }
+    if (chained) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -2944,6 +3027,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
                                                          const double *tmp)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     LeafCtl &ctl = *reinterpret_cast<LeafCtl *>(smem_raw + (kLeafSmem - sizeof(LeafCtl) - 64));
     if (abort_requested(st)) return;
@@ -2958,6 +3042,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
     const int lq_n = lq_nb + *reinterpret_cast<volatile int *>(&st->lq_claim);
     bool local_phase = true;   // (thread 0 only)
     for (;;) {
+        KS_TL_T0;
         if (threadIdx.x == 0) {
             int kind = -1;
             // 1. the plan's local partitions, biggest work first: one ticket each
@@ -2972,20 +3057,24 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
                     local_phase = false;
                 }
             }
-            // 2. the sort queue: take a ticket, wait until it is published or no work is left
+            // 2. the sort queue: take a ticket, wait until it is published or no
+            //    more can come (no local partition queued or running: during a
+            //    launch only those produce items -- hand-backs wait for the next
+            //    launch -- so the CTA leaves and its SM goes to the list sorters)
             if (kind < 0) {
                 const int idx = atomicAdd(&st->sq_head, 1);
+                const int slot = idx % Q.scap;
                 for (;;) {
-                    if (idx < ld_acquire_s32(&st->sq_claim)) {
-                        const int slot = idx % Q.scap;
-                        while (ld_acquire_u64(&Q.sq_ready[slot]) != q_tag(Q.epoch, idx)) __nanosleep(32);
+                    if (ld_acquire_u64(&Q.sq_ready[slot]) == q_tag(Q.epoch, idx)) {
                         const Seg *q = Q.sq + slot;
                         ctl.seg = load_item(q);
                         kind = __ldcg(&q->k);
                         break;
                     }
-                    if (ld_acquire_s32(&st->pending) == 0) break;   // nothing queued or running: done
-                    __nanosleep(128);
+                    if (idx >= ld_acquire_s32(&st->sq_claim) && ld_acquire_s32(&st->pending) == 0 &&
+                        idx >= ld_acquire_s32(&st->sq_claim))
+                        break;   // (claims are made before a partition leaves `pending`)
+                    __nanosleep(64);
                 }
             }
             ctl.kind = kind;
@@ -2993,8 +3082,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
         __syncthreads();
         KS_TR(13);   // item fetch (incl. waiting for work)
         const int kind = ctl.kind;
+        KS_TL(2, -1, kind);   // (kind -1: the final wait for pending == 0)
         if (kind < 0) break;
         const Seg g = ctl.seg;
+        {
+        KS_TL_T0;
         if (kind == kItemLocal) {
             local_one(*reinterpret_cast<LocalSmem *>(smem_raw), g, A, st, keys, tmp);
             KS_TR(14);
@@ -3008,8 +3100,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
             segs_sorted += 1;
             KS_TR(15);
         }
+        KS_TL(2, kind, g.len);
+        }
+        if (kind == kItemLocal) __threadfence();   // (its children and list entries before `pending` drops)
         __syncthreads();   // this item's children are published; smem free for the next one
-        if (threadIdx.x == 0) {
+        if (threadIdx.x == 0 && kind == kItemLocal) {
             __threadfence();
             atomicSub(&st->pending, 1);
         }
@@ -3022,6 +3117,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
         atomicAdd(&st->keys_leaf, keys_sorted);
         atomicAdd(&st->leaves, segs_sorted);
     }
+    KS_TL(2, 8, keys_sorted);
 }
 
 // ---------------------------------------------------------------------------
@@ -3176,6 +3272,22 @@ __global__ void k_set_ints(IntPtrs z)
     if (threadIdx.x < 8 && z.p[threadIdx.x]) *z.p[threadIdx.x] = 0;
 }
 
+// End of a leaf launch (all its sorters done): queue and list counters reset,
+// the sorters' hand-backs become the next launch's local items.
+__global__ void k_leaf_reset(LeafQ Q, DevStatus *st)
+{
+    KS_PDL_ENTRY();
+    const int nhb = min(st->nhb, Q.hb_cap);
+    for (int i = threadIdx.x; i < nhb; i += blockDim.x) Q.lq[Q.lcap - 1 - i] = with_kind(Q.hb[i], kItemLocal);
+    if (threadIdx.x == 0) {
+        st->lq_claim = nhb;
+        st->pending = nhb;
+        st->nhb = 0;
+        st->lq_head = st->lqb_claim = st->sq_claim = st->sq_head = 0;
+        st->nsmall[0] = st->nsmall[1] = st->small_next[0] = st->small_next[1] = st->nunits = 0;
+    }
+}
+
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 FastLayout fast_layout(long long n, long long nseg0)
@@ -3188,6 +3300,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.sq_cap = L.lq_cap;
     L.small_cap[0] = (int)(n / (kUnitMax + 1) + nseg0 + 2);      // disjoint ranges per leaf launch
     L.small_cap[1] = (int)(n / (sort_cap(0) + 1) + nseg0 + 2);
+    L.hb_cap = (int)(n / (kUnitMax + 1) + nseg0 + 2);              // hand-backs: disjoint ranges of > kUnitMax keys
     const long long psum = n / kKeysPerPivot + L.seg_cap + 1;    // sum of P_i over one global pass
     L.piv_cap = (int)(psum + L.seg_cap + 1);                     // + one NaN sentinel per segment
     L.lut_cap = (int)(16 * psum + kLutMax);                      // sum of T_i (T_i < 16 P_i)
@@ -3209,6 +3322,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.o_sq = off; off = align_up(off + sizeof(Seg) * L.sq_cap);
     L.o_small[0] = off; off = align_up(off + sizeof(Seg) * L.small_cap[0]);
     L.o_small[1] = off; off = align_up(off + sizeof(Seg) * L.small_cap[1]);
+    L.o_hb = off; off = align_up(off + sizeof(Seg) * L.hb_cap);
     L.o_chunk = off; off = align_up(off + sizeof(int) * L.ch_cap);
     L.o_piv = off; off = align_up(off + sizeof(double) * L.piv_cap);
     L.o_lut = off; off = align_up(off + sizeof(unsigned) * L.lut_cap);
@@ -3437,7 +3551,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     LeafQ Q{reinterpret_cast<Seg *>(w + L.o_lq), reinterpret_cast<unsigned long long *>(w + L.o_lq_ready), L.lq_cap,
             reinterpret_cast<Seg *>(w + L.o_sq), reinterpret_cast<unsigned long long *>(w + L.o_sq_ready), L.sq_cap,
             1, {reinterpret_cast<Seg *>(w + L.o_small[0]), reinterpret_cast<Seg *>(w + L.o_small[1])},
-            {L.small_cap[0], L.small_cap[1]}};
+            {L.small_cap[0], L.small_cap[1]}, reinterpret_cast<Seg *>(w + L.o_hb), L.hb_cap};
 
     const EngineCfg *cfg = engine_cfg();
     if (cfg == nullptr) return KS_CUDA_ERROR;
@@ -3615,23 +3729,19 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     auto leaf = [&]() {
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1, 0};
         K.run(kPhLeaf, [&] { launch_pdl(kPdlHeavy, k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
-        // queue claims reset before the small sorts (their hand-backs belong to the next epoch)
-        K.run(kPhGate, [&] {   // (bookkeeping launches are booked under "gate")
-            launch(k_set_ints, dim3(1), dim3(32), 0, stream,
-                   IntPtrs{{&st->lq_claim, &st->lq_head, &st->sq_claim, &st->sq_head, &st->lqb_claim, nullptr, nullptr,
-                            nullptr}});
-        });
-        LeafQ Qn = Q;
-        ++Qn.epoch;
+        // the list sorters: chained behind the leaf kernel (programmatic launch),
+        // their CTAs take the SMs the leaf's CTAs leave once no local partition is
+        // left (the lists are final then; see k_segsort).
         // class-1 list: on large inputs (many segments per CTA slot) the
         // single-buffer sorter (3 per SM, 256 threads) has the higher throughput;
         // on smaller ones the 512-thread sorter's shorter per-segment latency wins
         // (measured: 10M keys -2.4%, 500 x 100K -4.0%; 7M +4.4%, 1M +10%)
-        // the two lists are disjoint ranges: the class-0 sorter (which also finishes
-        // the warp units and fills) runs on the side stream next to the class-1
-        // sorter and fills the SMs the class-1 launch's tail leaves idle
-        // (measured: 100K keys -12%, 500 x 100K -2.3%; one array of 10M keys +1.8%
-        // -- there the class-1 list alone fills the GPU -- so not for large arrays)
+        // the two lists are disjoint ranges: on smaller inputs and batches the
+        // class-0 sorter (which also finishes the warp units and fills) runs on
+        // the side stream next to the class-1 sorter and fills the SMs the
+        // class-1 launch's tail leaves idle (measured: 100K keys -12%, 500 x 100K
+        // -2.3%); for one large array it is chained behind the class-1 sorter
+        const bool chain = KS_LEAF_CHAIN && !profile;
         const bool sort_fork = KS_SORT_FORK && !profile && (n < KS_SINGLE_MIN_N || d_off != nullptr);
         const ForkRes *fr = sort_fork ? fork_res() : nullptr;
         cudaStream_t s0 = stream;
@@ -3640,38 +3750,33 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             cudaStreamWaitEvent(fr->side, fr->fork, 0);
             s0 = fr->side;
         }
+        const int ch1 = chain ? 1 : 0, ch0 = (chain && s0 == stream) ? 1 : 0;
         if (n >= KS_SINGLE_MIN_N)
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sort_smem<3>(), stream,
-                           Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
+                launch_pdl(chain, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sort_smem<3>(), stream,
+                           Q.small[1], &st->nsmall[1], &st->small_next[1], Q, st, keys, tmp, units, ch1);
             });
         else
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sort_smem<1>(), stream,
-                           Q.small[1], &st->nsmall[1], &st->small_next[1], Qn, st, keys, tmp, units);
+                launch_pdl(chain, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sort_smem<1>(), stream,
+                           Q.small[1], &st->nsmall[1], &st->small_next[1], Q, st, keys, tmp, units, ch1);
             });
         if (n >= KS_SINGLE_MIN_N)   // (same trade-off for the class-0 list: 8 single-buffer sorters per SM)
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy && s0 == stream, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)),
-                           sort_smem<4>(), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
-                           units);
+                launch_pdl(ch0 != 0, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)), sort_smem<4>(), s0,
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], Q, st, keys, tmp, units, ch0);
             });
         else
             K.run(kPhLeaf, [&] {
-                launch_pdl(kPdlHeavy && s0 == stream, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)),
-                           sort_smem<0>(), s0, Q.small[0], &st->nsmall[0], &st->small_next[0], Qn, st, keys, tmp,
-                           units);
+                launch_pdl(ch0 != 0, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sort_smem<0>(), s0,
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], Q, st, keys, tmp, units, ch0);
             });
         if (fr != nullptr) {
             cudaEventRecord(fr->join, fr->side);
             cudaStreamWaitEvent(stream, fr->join, 0);
         }
-        K.run(kPhGate, [&] {
-            launch(k_set_ints, dim3(1), dim3(32), 0, stream,
-                   IntPtrs{{&st->nsmall[0], &st->nsmall[1], &st->small_next[0], &st->small_next[1], &st->nunits, nullptr,
-                            nullptr, nullptr}});
-        });
-        Q = Qn;
+        K.run(kPhGate, [&] { launch(k_leaf_reset, dim3(1), dim3(256), 0, stream, Q, st); });
+        ++Q.epoch;
         ++leaves_run;
     };
     CheckWords *cw = reinterpret_cast<CheckWords *>(w + L.o_check);
@@ -3789,5 +3894,20 @@ extern "C" int ks_trace_read(unsigned long long *out, int n, int reset)
         cudaMemcpyToSymbol(ks::g_trace, z, sizeof(z));
     }
     return 0;
+}
+#endif
+#ifdef KS_TIMELINE
+extern "C" int ks_timeline_read(unsigned long long *out, int max_records, int reset)
+{
+    unsigned n = 0;
+    cudaMemcpyFromSymbol(&n, ks::g_tl_n, sizeof(n));
+    if (n > (unsigned)ks::kTlCap) n = ks::kTlCap;
+    if ((int)n > max_records) n = max_records;
+    if (out && n) cudaMemcpyFromSymbol(out, ks::g_tl, 32ull * n);
+    if (reset) {
+        unsigned z = 0;
+        cudaMemcpyToSymbol(ks::g_tl_n, &z, sizeof(z));
+    }
+    return (int)n;
 }
 #endif

@@ -9,9 +9,9 @@ namespace ks {
 
 struct FastLayout {
     long long n;
-    int seg_cap, lq_cap, sq_cap, small_cap[2], piv_cap, lut_cap, ch_cap, unit_cap;
+    int seg_cap, lq_cap, sq_cap, small_cap[2], hb_cap, piv_cap, lut_cap, ch_cap, unit_cap;
     long long mat_cap, bsum_cap;
-    size_t o_status, o_seg[2], o_lq, o_lq_ready, o_sq, o_sq_ready, o_small[2], o_chunk, o_piv, o_lut, o_mat, o_moff, o_bsum, o_units, o_tmp, o_cls, o_check;
+    size_t o_status, o_seg[2], o_lq, o_lq_ready, o_sq, o_sq_ready, o_small[2], o_hb, o_chunk, o_piv, o_lut, o_mat, o_moff, o_bsum, o_units, o_tmp, o_cls, o_check;
     size_t total;
 };
 

@@ -160,7 +160,9 @@ struct DevStatus {
     int lq_claim, lq_head;            // local queue: slots claimed by producers / taken by consumers
     int lqb_claim;                    // ... big local items (> kLocalBig), stored from the front (LPT)
     int sq_claim, sq_head;            // sort queue
-    int pending;                      // queued or running leaf items (the leaf kernel ends at zero)
+    int pending;                      // local partitions queued or running (the only producers of leaf
+                                      // items during a leaf launch; its CTAs may leave once it is zero)
+    int nhb;                          // sorter hand-backs (skewed buckets), partitioned by the next leaf launch
     int nsmall[2];                    // small-segment lists (size classes 0, 1), sorted after the leaf launch
     int small_next[2];                // their work counters
     int nchunks;                      // chunks of the current level
