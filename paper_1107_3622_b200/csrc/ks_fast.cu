@@ -685,7 +685,6 @@ __global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, lo
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
-    KS_TL_T0;
     __shared__ long long sh[33];
     unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
     for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
@@ -698,7 +697,6 @@ __global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, lo
     __syncthreads();
     seg_offsets_body(Lst.gsegs, st->nseg[0], st, mat_cap, ch_cap, piv_cap, lut_cap, mat, moff, tstat, &st->nseg[1],
                      items, sh);
-    KS_TL(20, 8, 0);
     KS_TL(20, 8, 0);
 }
 
@@ -756,7 +754,6 @@ __global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const double *in, i
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
-    KS_TL_T0;
     __shared__ double x[kPMax + 1];
     constexpr int kU = (kPMax + 1 + kRankThreads - 1) / kRankThreads;   // all loads in flight at once
     double t[kU];
@@ -787,7 +784,6 @@ __global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const double *in, i
     for (int o = kRankParts / 2; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (i < P && part == 0) sorted[r] = v;   // (NaN keys -- rejected by the gate -- may collide; all in range)
     KS_TL(21, 8, 0);
-    KS_TL(21, 8, 0);
 }
 
 constexpr int kLutCtas = 16;
@@ -796,7 +792,6 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
                                                              unsigned *lut_pool, int *chunk_seg, unsigned *mat)
 {
     KS_PDL_ENTRY();
-    KS_TL_T0;
     KS_TL_T0;
     __shared__ double piv[kPMax + kPivPad];
     __shared__ long long sh[33];
@@ -849,7 +844,6 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
             segs[0].scale = scale;
         }
     }
-    KS_TL(22, 8, 0);
     KS_TL(22, 8, 0);
 }
 
@@ -1075,7 +1069,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
-    KS_TL_T0;
     constexpr unsigned long long kScanAgg = 1ull << 62, kScanPrefix = 2ull << 62, kScanVal = (1ull << 62) - 1;
     __shared__ long long sh[33];
     __shared__ int s_tile;
@@ -1158,7 +1151,6 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_lookback(const unsigned *
         }
         __syncthreads();   // s_tile / s_excl reuse
     }
-    KS_TL(24, 8, 0);
     KS_TL(24, 8, 0);
 }
 
@@ -1545,7 +1537,6 @@ __global__ void __launch_bounds__(kCount2Threads, KS_COUNT2_MINB) k_count2(const
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
-    KS_TL_T0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     CountSmem &CS = *reinterpret_cast<CountSmem *>(smem_raw);
     PassSmem &P = CS.P;
@@ -1608,7 +1599,6 @@ __global__ void __launch_bounds__(kCount2Threads, KS_COUNT2_MINB) k_count2(const
     }
     if (kGate) gate_flush(bad, pz, nz, st);
     KS_TL(23, 8, 0);
-    KS_TL(23, 8, 0);
 }
 
 struct Scatter2Smem {
@@ -1639,7 +1629,6 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
                                                               const unsigned short *cls, int pf)
 {
     KS_PDL_ENTRY();
-    KS_TL_T0;
     KS_TL_T0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Scatter2Smem &S = *reinterpret_cast<Scatter2Smem *>(smem_raw);
@@ -1858,7 +1847,6 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
 #if KS_SCAT_TMA
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 #endif
-    KS_TL(26, 8, 0);
     KS_TL(26, 8, 0);
 }
 
@@ -2124,7 +2112,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
-    KS_TL_T0;
     __shared__ long long sh[33];
     __shared__ long long sbase[5];
     __shared__ int s_mg[kPlanThreads];
@@ -2161,7 +2148,6 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
             account_partition(st, len, o, false);
         }
     }
-    KS_TL(25, 8, 0);
     KS_TL(25, 8, 0);
 }
 
