@@ -18,6 +18,7 @@
 // warp-per-unit finishing launch.  No key crosses to the host; the host reads
 // one small status block per pass to decide whether another pass is needed.
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <cstdio>
 #include <memory>
@@ -154,8 +155,8 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #define KS_SINGLE2 0      // the leaf's class-2 sorter with a single shared buffer (room for larger segments)
 #endif
 #ifndef KS_PLAN_FORK
-#define KS_PLAN_FORK 1    // the global plan runs concurrently with the scatter (data writes deferred to the finish pass)
-#endif
+#define KS_PLAN_FORK 2    // the global plan runs concurrently with the scatter (data writes deferred to the finish
+#endif                    // pass): 1 forked onto a side stream, 2 chained (PDL) into the scatter's tail
 #ifndef KS_SORT_FORK
 #define KS_SORT_FORK 1    // class-0 and class-1 list sorters run concurrently (side stream)
 #endif
@@ -170,6 +171,9 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #endif
 #ifndef KS_LEAF_CHAIN
 #define KS_LEAF_CHAIN 1   // the list sorters start (PDL) on the SMs the leaf kernel's CTAs leave
+#endif
+#ifndef KS_MAPPED_STATUS
+#define KS_MAPPED_STATUS 1   // the status block reaches the host through mapped memory (polled)
 #endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
@@ -259,7 +263,25 @@ struct LeafQ {
     int small_cap[2];
     Seg *hb;          // sorter hand-backs: partitioned by the next leaf launch (its local queue)
     int hb_cap;
+    unsigned *seq;    // call sequence word (CallSeq.seq): part of every ready tag
 };
+
+// Ready tags are (call sequence, leaf launch, claim index): a slot's word from an
+// earlier call or launch never matches, so the words need no clearing per call
+// (the init kernel clears them only for a fresh or re-laid-out workspace and
+// when the 27-bit sequence wraps).
+struct CallSeq {
+    unsigned seq;
+    unsigned pad_;
+    unsigned long long magic;   // workspace layout the ready words belong to
+};
+constexpr int kTagIdxBits = 25, kTagEpBits = 12;
+constexpr unsigned kSeqMask = (1u << (64 - kTagIdxBits - kTagEpBits)) - 1u;
+__device__ __forceinline__ unsigned long long q_epoch(const LeafQ &Q)
+{
+    const unsigned s = *reinterpret_cast<const volatile unsigned *>(Q.seq);
+    return ((unsigned long long)s << kTagEpBits) | (unsigned)(Q.epoch & ((1 << kTagEpBits) - 1));
+}
 
 // A skewed bucket the on-chip sorter cannot finish goes back to the first-key
 // partitioner in the NEXT leaf launch: no queue item appears during a launch
@@ -278,9 +300,9 @@ __device__ __forceinline__ void small_push(const LeafQ &Q, const Seg &g, DevStat
     if (i < Q.small_cap[c]) (c ? Q.small[1] : Q.small[0])[i] = g; else st->overflow = 5;
 }
 
-__device__ __forceinline__ unsigned long long q_tag(int epoch, int idx)
+__device__ __forceinline__ unsigned long long q_tag(unsigned long long ep, int idx)
 {
-    return ((unsigned long long)(unsigned)epoch << 32) | (unsigned)idx;
+    return (ep << kTagIdxBits) | (unsigned)idx;
 }
 
 __device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned long long v)
@@ -302,7 +324,7 @@ __device__ __forceinline__ int ld_acquire_s32(const int *p)
 
 // write the item, then release its tag (the item is visible before the tag)
 __device__ __forceinline__ void q_publish(Seg *q, unsigned long long *ready, int cap, int idx, const Seg &g,
-                                          int epoch)
+                                          unsigned long long epoch)
 {
     const int slot = idx % cap;
     q[slot] = g;
@@ -329,7 +351,7 @@ __device__ __forceinline__ void q_push1(bool local, const LeafQ &Q, const Seg &g
     }
     if (local) atomicAdd(&st->pending, 1);
     q_publish(Q.sq, Q.sq_ready, Q.scap, atomicAdd(&st->sq_claim, 1), with_kind(g, local ? kItemLocal : kItemSort),
-              Q.epoch);
+              q_epoch(Q));
 }
 
 // Initial routing of one array (or one segment of a batch).
@@ -359,9 +381,30 @@ __device__ __forceinline__ void route_initial(long long a, long long len, const 
 }
 
 // Single array: reset the status block and route the whole array (one launch).
-__global__ void k_init_single(long long n, InitLists Lst, DevStatus *st)
+// One CTA, before any queue item of the call is published: next call sequence
+// number; ready words cleared when the workspace is fresh / re-laid-out or the
+// sequence wraps.
+__device__ void seq_advance(const LeafQ &Q, unsigned long long magic)
+{
+    __shared__ int s_clear;
+    if (threadIdx.x == 0) {
+        CallSeq *c = reinterpret_cast<CallSeq *>(Q.seq);
+        unsigned sq = (c->seq + 1u) & kSeqMask;
+        s_clear = (c->magic != magic || sq == 0u) ? 1 : 0;
+        if (sq == 0u) sq = 1u;
+        c->seq = sq;
+        c->magic = magic;
+    }
+    __syncthreads();
+    if (s_clear)
+        for (int i = threadIdx.x; i < Q.scap; i += blockDim.x) Q.sq_ready[i] = 0ull;
+    __syncthreads();
+}
+
+__global__ void k_init_single(long long n, InitLists Lst, DevStatus *st, unsigned long long magic)
 {
     KS_PDL_ENTRY();
+    seq_advance(Lst.Q, magic);
     static_assert(sizeof(DevStatus) % 8 == 0, "status is cleared in 8-byte words");
     unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
     for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
@@ -681,9 +724,10 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
 // bookkeeping of k_seg_offsets in one launch.
 __global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, long long mat_cap, int ch_cap,
                                    int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
-                                   unsigned long long *tstat, int items)
+                                   unsigned long long *tstat, int items, unsigned long long magic)
 {
     KS_PDL_ENTRY();
+    seq_advance(Lst.Q, magic);
     KS_TL_T0;
     __shared__ long long sh[33];
     unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
@@ -846,6 +890,7 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
     }
     KS_TL(22, 8, 0);
 }
+
 
 // ---------------------------------------------------------------------------
 // count: per (segment, chunk) class histogram -> class-major count matrix
@@ -2054,12 +2099,12 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     }
     if (s_gap)
         q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, (int)(sbase[3] + pk_get(xpk, kPkS, 11)),
-                  with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemSort), A.Q.epoch);
+                  with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemSort), q_epoch(A.Q));
     if (l_gap) {
         const int i = (int)(sbase[1] + pk_get(xpk, kPkL, 11));
         Seg c = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal);
         c.stall = stall;
-        if (A.in_leaf) q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, i, c, A.Q.epoch);
+        if (A.in_leaf) q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, i, c, q_epoch(A.Q));
         else if (i < A.Q.lcap) A.Q.lq[A.Q.lcap - 1 - i] = c; else st->overflow = 7;   // (read after this launch)
     }
     if (lb_gap) {
@@ -2107,15 +2152,25 @@ constexpr int kPlanChunks = (kPMax + 1 + kPlanThreads - 1) / kPlanThreads;   // 
 
 // One CTA per (segment, chunk of kPlanThreads pivot pairs): gap 2j and
 // equality run 2j+1 for j in the chunk (j = k: the last gap).
+// chained: launched programmatically behind the scatter (deferred emission:
+// it needs only the scan and the pivots), it runs on the SMs the scatter's
+// CTAs leave; it completes only after the scatter (griddepcontrol.wait at the end).
 __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const int *nseg, const double *piv_pool,
-                                                       const long long *moff, EmitArgs A, DevStatus *st, int dst_id)
+                                                       const long long *moff, EmitArgs A, DevStatus *st, int dst_id,
+                                                       int chained)
 {
-    KS_PDL_ENTRY();
+    if (chained)
+        asm volatile("griddepcontrol.launch_dependents;" :::);
+    else
+        KS_PDL_ENTRY();
     KS_TL_T0;
     __shared__ long long sh[33];
     __shared__ long long sbase[5];
     __shared__ int s_mg[kPlanThreads];
-    if (abort_requested(st)) return;
+    if (abort_requested(st)) {
+        if (chained) asm volatile("griddepcontrol.wait;" ::: "memory");
+        return;
+    }
     const int ns = *nseg;
     const int j0 = blockIdx.y * kPlanThreads;
     for (int s = blockIdx.x; s < ns; s += gridDim.x) {
@@ -2149,6 +2204,7 @@ __global__ void __launch_bounds__(kPlanThreads) k_plan(const Seg *segs, const in
         }
     }
     KS_TL(25, 8, 0);
+    if (chained) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
 // ---------------------------------------------------------------------------
@@ -3039,6 +3095,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
     // the plan's local items (all published before this launch): a fixed set
     // (written by the plan, i.e. before this launch: big ones at the front, the rest at the back)
     const int lq_nb = *reinterpret_cast<volatile int *>(&st->lqb_claim);
+    const unsigned long long ep = q_epoch(Q);   // (thread 0: ready tags of this launch)
     const int lq_n = lq_nb + *reinterpret_cast<volatile int *>(&st->lq_claim);
     bool local_phase = true;   // (thread 0 only)
     for (;;) {
@@ -3065,7 +3122,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
                 const int idx = atomicAdd(&st->sq_head, 1);
                 const int slot = idx % Q.scap;
                 for (;;) {
-                    if (ld_acquire_u64(&Q.sq_ready[slot]) == q_tag(Q.epoch, idx)) {
+                    if (ld_acquire_u64(&Q.sq_ready[slot]) == q_tag(ep, idx)) {
                         const Seg *q = Q.sq + slot;
                         ctl.seg = load_item(q);
                         kind = __ldcg(&q->k);
@@ -3272,11 +3329,21 @@ __global__ void k_set_ints(IntPtrs z)
     if (threadIdx.x < 8 && z.p[threadIdx.x]) *z.p[threadIdx.x] = 0;
 }
 
+// Status block mirrored into mapped (zero-copy) host memory by the last kernel
+// of a leaf launch, then a release of `flag`: the host polls the flag instead
+// of queueing a device-to-host copy and synchronising the stream.
+struct HostStatus {
+    DevStatus st;
+    unsigned long long flag;
+};
+
 // End of a leaf launch (all its sorters done): queue and list counters reset,
-// the sorters' hand-backs become the next launch's local items.
-__global__ void k_leaf_reset(LeafQ Q, DevStatus *st)
+// the sorters' hand-backs become the next launch's local items; the status
+// goes to the host when `out` is set.
+__global__ void k_leaf_reset(LeafQ Q, DevStatus *st, HostStatus *out)
 {
     KS_PDL_ENTRY();
+    KS_TL_T0;
     const int nhb = min(st->nhb, Q.hb_cap);
     for (int i = threadIdx.x; i < nhb; i += blockDim.x) Q.lq[Q.lcap - 1 - i] = with_kind(Q.hb[i], kItemLocal);
     if (threadIdx.x == 0) {
@@ -3286,6 +3353,17 @@ __global__ void k_leaf_reset(LeafQ Q, DevStatus *st)
         st->lq_head = st->lqb_claim = st->sq_claim = st->sq_head = 0;
         st->nsmall[0] = st->nsmall[1] = st->small_next[0] = st->small_next[1] = st->nunits = 0;
     }
+    if (out != nullptr) {
+        __syncthreads();
+        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(st);
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(&out->st);
+        for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) dst[i] = src[i];
+        __threadfence_system();
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&out->flag), "l"(1ull) : "memory");
+    }
+    KS_TL(27, 8, 0);
 }
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -3313,7 +3391,7 @@ FastLayout fast_layout(long long n, long long nseg0)
     L.unit_cap = (int)(2 * (n / (kTinyGap + 1)) + n / kFillPiece + nseg0 + 4096);
     L.bsum_cap = cdiv(L.mat_cap, kScanBlock) + 1;
     size_t off = 0;
-    L.o_status = off; off = align_up(off + sizeof(DevStatus));
+    L.o_status = off; off = align_up(off + sizeof(DevStatus) + sizeof(CallSeq));   // (CallSeq right behind)
     L.o_seg[0] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
     L.o_seg[1] = off; off = align_up(off + sizeof(Seg) * L.seg_cap);
     L.o_lq_ready = off; off = align_up(off + sizeof(unsigned long long) * L.lq_cap);   // (ready words contiguous:
@@ -3408,10 +3486,11 @@ struct GraphKey {
     const void *keys, *d_off, *ws;
     long long n, nseg0;
     size_t ws_bytes;
+    const void *hs;   // the calling thread's mapped status block (baked into the graph)
     bool operator==(const GraphKey &o) const
     {
         return keys == o.keys && d_off == o.d_off && ws == o.ws && n == o.n && nseg0 == o.nseg0 &&
-               ws_bytes == o.ws_bytes;
+               ws_bytes == o.ws_bytes && hs == o.hs;
     }
 };
 // The executable graph is reference-counted: a thread that evicts an entry
@@ -3479,6 +3558,38 @@ struct PinnedStatus {
         if (p) cudaFreeHost(p);
     }
 };
+// Per host thread: a mapped pinned status block (the graph bakes its device
+// address in; the graph key carries it, so a graph only ever signals the
+// thread that captured it).
+struct MappedStatus {
+    HostStatus *h = nullptr;
+    HostStatus *d = nullptr;
+    ~MappedStatus()
+    {
+        if (h) cudaFreeHost(h);
+    }
+};
+static MappedStatus *mapped_status()
+{
+    static thread_local MappedStatus ms;
+    if (ms.h == nullptr) {
+        HostStatus *h = nullptr;
+        if (cudaHostAlloc(reinterpret_cast<void **>(&h), sizeof(HostStatus), cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        HostStatus *d = nullptr;
+        if (cudaHostGetDevicePointer(reinterpret_cast<void **>(&d), h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFreeHost(h);
+            return nullptr;
+        }
+        ms.h = h;
+        ms.d = d;
+    }
+    return &ms;
+}
+
 static DevStatus *pinned_status()
 {
     static thread_local PinnedStatus ps;
@@ -3536,6 +3647,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     cudaStream_t stream = user_stream;   // (the capture stream while a graph is being recorded)
     FastLayout L = fast_layout(n, nseg0);
     if (ws_bytes < L.total) return KS_WORKSPACE_SMALL;
+    if (L.sq_cap >= (1 << kTagIdxBits)) return KS_BAD_ARG;   // (ready tags hold 25-bit claim indices: n < 1.7e10)
     char *w = static_cast<char *>(ws);
     DevStatus *st = reinterpret_cast<DevStatus *>(w + L.o_status);
     Seg *segs[2] = {reinterpret_cast<Seg *>(w + L.o_seg[0]), reinterpret_cast<Seg *>(w + L.o_seg[1])};
@@ -3551,7 +3663,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     LeafQ Q{reinterpret_cast<Seg *>(w + L.o_lq), reinterpret_cast<unsigned long long *>(w + L.o_lq_ready), L.lq_cap,
             reinterpret_cast<Seg *>(w + L.o_sq), reinterpret_cast<unsigned long long *>(w + L.o_sq_ready), L.sq_cap,
             1, {reinterpret_cast<Seg *>(w + L.o_small[0]), reinterpret_cast<Seg *>(w + L.o_small[1])},
-            {L.small_cap[0], L.small_cap[1]}, reinterpret_cast<Seg *>(w + L.o_hb), L.hb_cap};
+            {L.small_cap[0], L.small_cap[1]}, reinterpret_cast<Seg *>(w + L.o_hb), L.hb_cap,
+            reinterpret_cast<unsigned *>(w + L.o_status + sizeof(DevStatus))};
+    // workspace layout signature (ready words of another layout are stale)
+    const unsigned long long ws_magic = 0x4b53525459ull ^ ((unsigned long long)n * 0x9E3779B97F4A7C15ull) ^
+                                        ((unsigned long long)nseg0 << 40) ^ (unsigned long long)L.total;
 
     const EngineCfg *cfg = engine_cfg();
     if (cfg == nullptr) return KS_CUDA_ERROR;
@@ -3568,8 +3684,37 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 
     DevStatus h{};
     DevStatus *hp = pinned_status();   // (a pageable destination would add a staged copy)
+    // device calls end with the status in mapped host memory (polled; no copy,
+    // no stream synchronisation); host destinations (h_out) still synchronise
+    // for their copy, profiled calls keep the plain path
+    MappedStatus *ms = (KS_MAPPED_STATUS && h_out == nullptr && !profile && !KS_CHECK) ? mapped_status() : nullptr;
+    HostStatus *hs_dev = ms ? ms->d : nullptr;
+    volatile unsigned long long *hs_flag = ms ? &ms->h->flag : nullptr;
+    if (hs_flag) *hs_flag = 0ull;
     auto sync_status = [&]() -> int {
         KS_CK(cudaGetLastError());
+        if (hs_flag != nullptr) {
+            bool got = false;
+            for (unsigned it = 1;; ++it) {
+                if (*hs_flag != 0ull) {
+                    got = true;
+                    break;
+                }
+                if ((it & 255u) == 0u) {   // a failed launch never raises the flag
+                    const cudaError_t q = cudaStreamQuery(stream);
+                    if (q == cudaErrorNotReady) continue;
+                    if (q != cudaSuccess) return KS_CUDA_ERROR;
+                    got = *hs_flag != 0ull;
+                    break;
+                }
+            }
+            std::atomic_thread_fence(std::memory_order_acquire);
+            if (got) {
+                h = ms->h->st;
+                *hs_flag = 0ull;   // (armed for the next leaf launch of this call)
+                return (h.overflow && !h.bad_arg) ? KS_CUDA_ERROR : KS_OK;
+            }
+        }
         KS_CK(cudaMemcpyAsync(hp ? hp : &h, st, sizeof(DevStatus), cudaMemcpyDeviceToHost, stream));
         KS_CK(cudaStreamSynchronize(stream));
         if (hp) h = *hp;
@@ -3591,10 +3736,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         });
     };
     auto init_launch = [&]() {
-        // queue ready words: cleared once per call (their tags carry the leaf epoch)
-        cudaMemsetAsync(Q.lq_ready, 0, L.o_lq - L.o_lq_ready, stream);
-        if (d_off != nullptr) {   // (the single-array init kernel clears the status itself)
-            cudaMemsetAsync(st, 0, sizeof(DevStatus), stream);
+        // batches: queue ready words cleared here, status and call sequence reset
+        // (a single array: the init kernel advances the call sequence instead)
+        if (d_off != nullptr) {
+            cudaMemsetAsync(Q.sq_ready, 0, sizeof(unsigned long long) * L.sq_cap, stream);
+            cudaMemsetAsync(st, 0, sizeof(DevStatus) + sizeof(CallSeq), stream);
             cudaMemsetAsync(&st->bad_index, 0xff, sizeof(unsigned long long), stream);
         }
         if (d_off == nullptr) {
@@ -3609,7 +3755,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                 K.run(kPhGate, [&] {
                     launch(k_init_single_pass, dim3(1), dim3(1024), 0, stream, n, Lst, st, L.mat_cap, L.ch_cap,
                            L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum),
-                           pass_items);
+                           pass_items, ws_magic);
                 });
                 if (fr != nullptr) {
                     cudaEventRecord(fr->join, fr->side);
@@ -3617,7 +3763,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                     rank_done = true;
                 }
             } else
-                K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st); });
+                K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st, ws_magic); });
             if (n <= kInitLocalMax)
                 K.run(kPhGate, [&] { launch(k_gate_segments, dim3(sms * 2), dim3(256), 0, stream, keys, nullptr, 0, n, n, st); });
         } else {
@@ -3642,8 +3788,9 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
         const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
-        const ForkRes *fr = (KS_PLAN_FORK && !profile) ? fork_res() : nullptr;
-        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, fr ? 1 : 0};
+        const int plan_mode = profile ? 0 : KS_PLAN_FORK;
+        const ForkRes *fr = plan_mode == 1 ? fork_res() : nullptr;
+        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, plan_mode ? 1 : 0};
         if (!(level == 0 && d_off == nullptr))   // (done by k_init_single_pass)
             K.run(kPhPivots, [&] {
                 launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
@@ -3709,16 +3856,18 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             cudaStreamWaitEvent(fr->side, fr->fork, 0);
             K.run(kPhPlan, [&] {
                 launch_pdl(false, k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, fr->side, segs[gcur], nseg_cur, piv,
-                           moff, A, st, dst_id);
+                           moff, A, st, dst_id, 0);
             });
             launch_scatter();
             cudaEventRecord(fr->join, fr->side);
             cudaStreamWaitEvent(stream, fr->join, 0);
         } else {
+            // (chained: the plan's CTAs take the SMs the scatter's leave -- forked, they
+            // held 16 SMs at the scatter's start and those scatter CTAs ended 10 us late)
             launch_scatter();
             K.run(kPhPlan, [&] {
                 launch(k_plan, dim3(gx, kPlanChunks), dim3(kPlanThreads), 0, stream, segs[gcur], nseg_cur, piv, moff, A,
-                       st, dst_id);
+                       st, dst_id, plan_mode == 2 ? 1 : 0);
             });
         }
         ++level;
@@ -3728,6 +3877,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // CTA shapes (hand-backs go to the next leaf epoch), the warp units and fills
     auto leaf = [&]() {
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1, 0};
+        if ((Q.epoch & ((1 << kTagEpBits) - 1)) == 0)   // (4096 leaf launches in one call: the tags' epoch wraps)
+            cudaMemsetAsync(Q.sq_ready, 0, sizeof(unsigned long long) * L.sq_cap, stream);
         K.run(kPhLeaf, [&] { launch_pdl(kPdlHeavy, k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // the list sorters: chained behind the leaf kernel (programmatic launch),
         // their CTAs take the SMs the leaf's CTAs leave once no local partition is
@@ -3775,7 +3926,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             cudaEventRecord(fr->join, fr->side);
             cudaStreamWaitEvent(stream, fr->join, 0);
         }
-        K.run(kPhGate, [&] { launch(k_leaf_reset, dim3(1), dim3(256), 0, stream, Q, st); });
+        K.run(kPhGate, [&] { launch(k_leaf_reset, dim3(1), dim3(256), 0, stream, Q, st, hs_dev); });
         ++Q.epoch;
         ++leaves_run;
     };
@@ -3793,7 +3944,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     bool replayed = false;
     if (KS_GRAPH && !profile) {
         // the speculative schedule depends only on (buffers, sizes): replay it as one CUDA graph
-        const GraphKey key{keys, d_off, ws, n, nseg0, ws_bytes};
+        const GraphKey key{keys, d_off, ws, n, nseg0, ws_bytes, hs_dev};
         GraphEntry e{};
         bool seen = false;
         bool have = graph_lookup(key, &e, &seen);
@@ -3897,6 +4048,18 @@ extern "C" int ks_trace_read(unsigned long long *out, int n, int reset)
 }
 #endif
 #ifdef KS_TIMELINE
+namespace ks {
+__global__ void k_tl_mark(int id)
+{
+    KS_TL_T0;
+    KS_TL(id, 8, 0);
+}
+}  // namespace ks
+extern "C" int ks_timeline_mark(void *stream, int id)
+{
+    ks::k_tl_mark<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(id);
+    return (int)cudaGetLastError();
+}
 extern "C" int ks_timeline_read(unsigned long long *out, int max_records, int reset)
 {
     unsigned n = 0;

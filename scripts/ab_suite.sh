@@ -2,7 +2,7 @@
 # A/B device timing of exp/lib_*.so builds over the BASELINE single-array configs.
 #   gpurun -- 'bash scripts/ab_suite.sh exp/lib_a.so exp/lib_b.so'
 LIBS=("$@")
-for cfg in "10000000 uniform01" "7000000 uniform01" "1000000 uniform01" "10000000 dup256"; do
+for cfg in "10000000 uniform01" "7000000 uniform01" "1000000 uniform01" "100000 uniform01" "10000000 dup256"; do
   set -- $cfg; n=$1; k=$2; shift 2
   echo "== n=$n kind=$k"
   EXP_N=$n EXP_KIND=$k EXP_REPS=${EXP_REPS:-30} timeout 300 python scripts/ab_time.py "${LIBS[@]}" 2>&1 | grep "^{"

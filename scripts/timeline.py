@@ -32,14 +32,23 @@ cap = 1 << 17
 buf = (ctypes.c_ulonglong * (4 * cap))()
 p = K.generate_device(n, 20260816, kind)
 k = torch.empty_like(p)
-flush = torch.empty(32 * 1024 * 1024, dtype=torch.float64, device="cuda")
+flush = torch.empty(int(os.environ.get("TL_FLUSH_MB", "256")) * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+L.ks_timeline_mark.argtypes = [ctypes.c_void_p, ctypes.c_int]
+sp = torch.cuda.current_stream().cuda_stream
 for rep in range(4):
     k.copy_(p)
     flush.zero_()
     torch.cuda.synchronize()
     L.ks_timeline_read(None, 0, 1)
+    flush.zero_()                 # (the GPU is busy while the call is issued, as in bench.py)
+    L.ks_timeline_mark(sp, 30)    # mark: the flush has ended
+    ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ea.record()
     K.k_sort(k)
+    eb.record()
+    L.ks_timeline_mark(sp, 31)    # mark: enqueued after the call returned
     torch.cuda.synchronize()
+    ev_ms = ea.elapsed_time(eb)
 m = L.ks_timeline_read(ctypes.addressof(buf), cap, 0)
 assert torch.equal(k, torch.sort(p).values)
 recs = []
@@ -51,9 +60,15 @@ T0 = min(r["t0"] for r in recs)
 for r in recs:
     r["t0"] -= T0
     r["t1"] -= T0
-names = {2: "k_leaf", 10: "segsort<0>", 11: "segsort<1>", 13: "segsort<3>", 14: "segsort<4>", 20: "init_pass",
-         21: "pivot_rank", 22: "pivot_lut", 23: "count2", 24: "scan", 25: "plan", 26: "scatter2"}
-print(f"n={n} kind={kind} records={m}")
+names = {30: "mark0", 31: "mark1", 2: "k_leaf", 10: "segsort<0>", 11: "segsort<1>", 13: "segsort<3>", 14: "segsort<4>", 20: "init_pass",
+         21: "pivot_rank", 22: "pivot_lut", 23: "count2", 24: "scan", 25: "plan", 26: "scatter2", 27: "leaf_reset"}
+print(f"n={n} kind={kind} records={m} event span {ev_ms*1e3:.1f} us")
+mk = {r["kernel"]: r for r in recs if r["kernel"] in (30, 31)}
+if 30 in mk and 31 in mk:
+    first = min(r["t0"] for r in recs if r["kernel"] not in (30, 31))
+    last = max(r["t1"] for r in recs if r["kernel"] not in (30, 31))
+    print(f"  mark(before) end {mk[30]['t1']/1e3:.1f} us -> first kernel {first/1e3:.1f} us; last kernel end "
+          f"{last/1e3:.1f} us -> mark(after) start {mk[31]['t0']/1e3:.1f} us")
 for kern in sorted({r["kernel"] for r in recs}):
     cta = [r for r in recs if r["kernel"] == kern and r["kind"] == 8]
     items = [r for r in recs if r["kernel"] == kern and r["kind"] in (0, 1)]
