@@ -62,6 +62,9 @@ typedef struct ks_status {
     float phase_ms[8];
     int32_t phase_launches[8];
     uint64_t phase_bytes[8];    /* algorithmic bytes of each phase (reads + writes) */
+    int32_t host_syncs;         /* times the call waited for the device (1 = the whole recursion ran
+                                 * device-resident behind one status read) */
+    int32_t reserved_;
 } ks_status_t;
 
 /* Workspace bytes needed to sort n_total keys held in n_segments segments

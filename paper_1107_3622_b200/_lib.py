@@ -48,6 +48,8 @@ class KsStatus(ctypes.Structure):
         ("phase_ms", ctypes.c_float * 8),
         ("phase_launches", ctypes.c_int32 * 8),
         ("phase_bytes", ctypes.c_uint64 * 8),
+        ("host_syncs", ctypes.c_int32),
+        ("reserved_", ctypes.c_int32),
     ]
 
     def as_dict(self) -> dict:

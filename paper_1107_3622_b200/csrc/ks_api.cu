@@ -23,6 +23,7 @@ void copy_fast(ks_status_t *s, const FastResult &r)
     s->keys_leaf_sorted = r.keys_leaf;
     s->leaves = r.leaves;
     s->launches = r.launches;
+    s->host_syncs = r.host_syncs;
     for (int p = 0; p < 8; ++p) {
         s->phase_ms[p] = r.phase_ms[p];
         s->phase_launches[p] = r.phase_launches[p];

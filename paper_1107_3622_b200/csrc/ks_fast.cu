@@ -175,6 +175,9 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #ifndef KS_MAPPED_STATUS
 #define KS_MAPPED_STATUS 1   // the status block reaches the host through mapped memory (polled)
 #endif
+#ifndef KS_DEVICE_LOOP
+#define KS_DEVICE_LOOP 1   // graph path: the remaining levels run in a conditional WHILE node (no host round
+#endif                     // trip) -- 1: for keys whose sorts needed it before, 2: always, 0: never
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
 #endif
@@ -688,6 +691,7 @@ __device__ void seg_offsets_body(Seg *segs, int ns, DevStatus *st, long long mat
         c_ch += tc;
     }
     if (threadIdx.x == 0) {
+        if (ns > 0) ++st->npasses;
         st->nchunks = (int)c_ch;
         st->chunk = (int)chunk;
         st->mat_total = c_mat;
@@ -3296,10 +3300,15 @@ class Launcher {
 // scheduled while its predecessor runs; KS_PDL_ENTRY() in every kernel waits
 // for the predecessor's completion before touching its results.
 constexpr bool kPdlHeavy = KS_PDL_HEAVY != 0;
+// set while the device loop's body is captured: a conditional body holds plain
+// kernel / memset nodes only (no programmatic edges, no forked side streams)
+static thread_local bool t_in_body = false;
+
 template <typename... KArgs, typename... Args>
 static cudaError_t launch_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t stream, Args &&...args)
 {
+    if (t_in_body) pdl = false;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -3337,10 +3346,25 @@ struct HostStatus {
     unsigned long long flag;
 };
 
+// status block -> mapped host memory, then the flag (one CTA, all threads)
+__device__ void publish_status(const DevStatus *st, HostStatus *out)
+{
+    __syncthreads();
+    const unsigned long long *src = reinterpret_cast<const unsigned long long *>(st);
+    unsigned long long *dst = reinterpret_cast<unsigned long long *>(&out->st);
+    for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) dst[i] = src[i];
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&out->flag), "l"(1ull) : "memory");
+}
+
 // End of a leaf launch (all its sorters done): queue and list counters reset,
-// the sorters' hand-backs become the next launch's local items; the status
-// goes to the host when `out` is set.
-__global__ void k_leaf_reset(LeafQ Q, DevStatus *st, HostStatus *out)
+// the sorters' hand-backs become the next launch's local items.  The host gets
+// the status (`out`): after every launch (host loop), or -- under the device
+// loop (`use_cond`: this kernel also sets the WHILE node's condition) -- once,
+// when no work is left.  gnext: the next level's segment table.
+__global__ void k_leaf_reset(LeafQ Q, DevStatus *st, HostStatus *out, cudaGraphConditionalHandle cond, int use_cond,
+                             int gnext)
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
@@ -3352,17 +3376,21 @@ __global__ void k_leaf_reset(LeafQ Q, DevStatus *st, HostStatus *out)
         st->nhb = 0;
         st->lq_head = st->lqb_claim = st->sq_claim = st->sq_head = 0;
         st->nsmall[0] = st->nsmall[1] = st->small_next[0] = st->small_next[1] = st->nunits = 0;
+        ++st->nleaves;
     }
-    if (out != nullptr) {
-        __syncthreads();
-        const unsigned long long *src = reinterpret_cast<const unsigned long long *>(st);
-        unsigned long long *dst = reinterpret_cast<unsigned long long *>(&out->st);
-        for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) dst[i] = src[i];
-        __threadfence_system();
-        __syncthreads();
-        if (threadIdx.x == 0)
-            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&out->flag), "l"(1ull) : "memory");
+    // Device-resident recursion (the reference's worklist, sort_core.py:184-198):
+    // more levels while segments or hand-backs are left and the call stands
+    __shared__ int s_pub;
+    if (threadIdx.x == 0) {
+        const bool ab = st->bad_index != kNoIndex || (st->pos_zero && st->neg_zero) || st->bad_arg || st->overflow;
+        const bool more = !ab && (st->nseg[gnext] > 0 || nhb > 0);
+        if (use_cond) cudaGraphSetConditional(cond, more ? 1u : 0u);
+        st->done = more ? 0 : 1;
+        s_pub = out != nullptr && (!use_cond || (!more && !st->published));
+        if (s_pub && use_cond) st->published = 1;
     }
+    __syncthreads();
+    if (s_pub) publish_status(st, out);
     KS_TL(27, 8, 0);
 }
 
@@ -3501,6 +3529,7 @@ struct GraphEntry {
     int dev;
     GraphExecPtr exec;
     int level, gcur, leaves_run, epoch, launches;
+    bool has_loop;   // the recursion's remaining levels run in a WHILE node
     unsigned long long last_use;
 };
 static std::mutex g_graph_mu;
@@ -3534,6 +3563,33 @@ static bool graph_lookup(const GraphKey &k, GraphEntry *out, bool *seen_before)
         ++seen_next;
     }
     return false;
+}
+
+// Keys whose sorts needed more than the speculative levels (presorted,
+// reversed, organ-pipe ... inputs): their graphs carry the device loop.  Other
+// graphs leave it out -- its WHILE node costs ~5 us per call (measured: C0
+// 0.321 -> 0.329 ms) -- and fall back to the host loop if ever needed, which
+// marks the key and drops the graph so that the next call recaptures it.
+static std::vector<std::pair<GraphKey, int>> g_loop_keys;
+static bool key_wants_loop(const GraphKey &k, int dev)
+{
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (auto &x : g_loop_keys)
+        if (x.first == k && x.second == dev) return true;
+    return false;
+}
+static void key_mark_loop(const GraphKey &k, int dev)
+{
+    std::lock_guard<std::mutex> lock(g_graph_mu);
+    for (size_t i = 0; i < g_graphs.size(); ++i)
+        if (g_graphs[i].dev == dev && g_graphs[i].key == k && !g_graphs[i].has_loop) {
+            g_graphs.erase(g_graphs.begin() + i);
+            break;
+        }
+    for (auto &x : g_loop_keys)
+        if (x.first == k && x.second == dev) return;
+    if (g_loop_keys.size() >= 4 * kGraphCacheMax) g_loop_keys.erase(g_loop_keys.begin());
+    g_loop_keys.emplace_back(k, dev);
 }
 
 static void graph_store(GraphEntry e)
@@ -3608,6 +3664,7 @@ struct ForkRes {
 };
 static const ForkRes *fork_res()
 {
+    if (t_in_body) return nullptr;
     static thread_local ForkRes res[64];
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
@@ -3640,6 +3697,20 @@ static cudaStream_t capture_stream()
     }
     return cs[dev].s;
 }
+
+static cudaStream_t body_stream()   // captures the device loop's body (per thread and device)
+{
+    static thread_local CaptureStream cs[64];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    if (cs[dev].s == nullptr && cudaStreamCreateWithFlags(&cs[dev].s, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        cs[dev].s = nullptr;
+    }
+    return cs[dev].s;
+}
+static std::atomic<int> g_dloop_broken{0};   // a failed device-loop capture: graphs without it from then on
+static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
               cudaStream_t user_stream, bool profile, FastResult *res, double *h_out)
@@ -3691,8 +3762,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     HostStatus *hs_dev = ms ? ms->d : nullptr;
     volatile unsigned long long *hs_flag = ms ? &ms->h->flag : nullptr;
     if (hs_flag) *hs_flag = 0ull;
+    int syncs = 0;
     auto sync_status = [&]() -> int {
         KS_CK(cudaGetLastError());
+        ++syncs;
         if (hs_flag != nullptr) {
             bool got = false;
             for (unsigned it = 1;; ++it) {
@@ -3778,6 +3851,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // the end; inputs that need more global passes (adversarial shapes:
     // presorted, few distinct values, ...) continue in a synchronising loop.
     int level = 0, gcur = 0, leaves_run = 0;
+    cudaGraphConditionalHandle cond_h{};
+    bool cond_on = false;            // capturing the device loop: k_leaf_reset sets its condition
+    // queue ready words cleared before a level (its plan publishes sort items)
+    auto clear_ready = [&]() { cudaMemsetAsync(Q.sq_ready, 0, sizeof(unsigned long long) * L.sq_cap, stream); };
     const int scatter_pf = n >= KS_PF_MIN_N ? 1 : 0;
     auto global_pass = [&]() {
         const double *src = (level & 1) ? tmp : keys;
@@ -3785,19 +3862,22 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const int dst_id = (level & 1) ? 0 : 1;
         int *nseg_cur = &st->nseg[gcur];
         // segments at this level: known on the host at level 0, else bounded by the table size
+        // (level 0 of one large array: its layout comes from k_init_single_pass; a
+        // small array's first pass -- only ever the device loop's no-op -- is generic)
+        const bool first_single = level == 0 && d_off == nullptr && n > kInitLocalMax;
         const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
         const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
-        const int plan_mode = profile ? 0 : KS_PLAN_FORK;
+        const int plan_mode = (profile || t_in_body) ? 0 : KS_PLAN_FORK;
         const ForkRes *fr = plan_mode == 1 ? fork_res() : nullptr;
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, plan_mode ? 1 : 0};
-        if (!(level == 0 && d_off == nullptr))   // (done by k_init_single_pass)
+        if (!first_single)   // (done by k_init_single_pass)
             K.run(kPhPivots, [&] {
                 launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
                        L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next,
                        pass_items);
             });
-        if (level == 0 && d_off == nullptr) {   // one segment, known P: build the pivots GPU-wide
+        if (first_single) {   // one segment, known P: build the pivots GPU-wide
             double *sorted = reinterpret_cast<double *>(moff);   // (scratch: the offsets are written later)
             if (!rank_done) launch_rank(stream);
             K.run(kPhPivots, [&] {
@@ -3875,10 +3955,11 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     };
     // leaf launch: queues -> sorted ranges; then the small segments by their own
     // CTA shapes (hand-backs go to the next leaf epoch), the warp units and fills
-    auto leaf = [&]() {
+    // sig: mapped status block the launch's last kernel signals (nullptr: none);
+    // clear: the queue's ready words are cleared first (a launch whose epoch
+    // may repeat: the device loop's body, the host loop after a replay)
+    auto leaf = [&](HostStatus *sig) {
         EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1, 0};
-        if ((Q.epoch & ((1 << kTagEpBits) - 1)) == 0)   // (4096 leaf launches in one call: the tags' epoch wraps)
-            cudaMemsetAsync(Q.sq_ready, 0, sizeof(unsigned long long) * L.sq_cap, stream);
         K.run(kPhLeaf, [&] { launch_pdl(kPdlHeavy, k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // the list sorters: chained behind the leaf kernel (programmatic launch),
         // their CTAs take the SMs the leaf's CTAs leave once no local partition is
@@ -3892,7 +3973,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         // the side stream next to the class-1 sorter and fills the SMs the
         // class-1 launch's tail leaves idle (measured: 100K keys -12%, 500 x 100K
         // -2.3%); for one large array it is chained behind the class-1 sorter
-        const bool chain = KS_LEAF_CHAIN && !profile;
+        const bool chain = KS_LEAF_CHAIN && !profile && !t_in_body;
         const bool sort_fork = KS_SORT_FORK && !profile && (n < KS_SINGLE_MIN_N || d_off != nullptr);
         const ForkRes *fr = sort_fork ? fork_res() : nullptr;
         cudaStream_t s0 = stream;
@@ -3926,10 +4007,14 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             cudaEventRecord(fr->join, fr->side);
             cudaStreamWaitEvent(stream, fr->join, 0);
         }
-        K.run(kPhGate, [&] { launch(k_leaf_reset, dim3(1), dim3(256), 0, stream, Q, st, hs_dev); });
+        K.run(kPhGate, [&] {
+            launch(k_leaf_reset, dim3(1), dim3(256), 0, stream, Q, st, sig, cond_h, cond_on ? 1 : 0, gcur);
+        });
         ++Q.epoch;
         ++leaves_run;
     };
+    HostStatus *sig_spec = hs_dev;   // the status block the schedule's leaf launches signal
+    bool dloop_failed = false;
     CheckWords *cw = reinterpret_cast<CheckWords *>(w + L.o_check);
     auto spec = [&]() {
         if (KS_CHECK) {
@@ -3938,7 +4023,53 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         }
         init_launch();
         if (n > kInitLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
-        leaf();
+        leaf(sig_spec);
+    };
+    // The rest of the recursion on the device (graph path): a WHILE node whose
+    // body runs two more levels (global pass + leaf launch at each parity) as
+    // long as k_more finds work; the body's kernels exit at once when a level
+    // has nothing to do.
+    auto capture_device_loop = [&](cudaStream_t cs) {
+        cudaStreamCaptureStatus cst_ = cudaStreamCaptureStatusNone;
+        cudaGraph_t g = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        if (cudaStreamGetCaptureInfo(cs, &cst_, nullptr, &g, &deps, &nd) != cudaSuccess) {
+            dloop_failed = true;
+            return;
+        }
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = cond_h;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t wn = nullptr;
+        if (cudaGraphAddNode(&wn, g, deps, nd, &np) != cudaSuccess ||
+            cudaStreamUpdateCaptureDependencies(cs, &wn, 1, cudaStreamSetCaptureDependencies) != cudaSuccess) {
+            dloop_failed = true;
+            return;
+        }
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        cudaStream_t bs = body_stream();
+        if (bs == nullptr || cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0,
+                                                           cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            dloop_failed = true;
+            return;
+        }
+        stream = bs;
+        t_in_body = true;
+        for (int half = 0; half < 2; ++half) {   // (each leaf launch's reset updates the condition)
+            clear_ready();   // (this epoch value repeats each iteration)
+            global_pass();
+            leaf(hs_dev);
+        }
+        t_in_body = false;
+        cudaGraph_t bg = body;
+        if (cudaStreamEndCapture(bs, &bg) != cudaSuccess) {
+            dloop_failed = true;
+            cudaGetLastError();
+        }
+        stream = cs;
     };
     int launches_graph = 0;
     bool replayed = false;
@@ -3954,18 +4085,42 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             e.key = key;
             stream = cs;
             KS_CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+            int dev_ = 0;
+            cudaGetDevice(&dev_);
+            bool dloop = KS_DEVICE_LOOP && device_loop_ok() && (KS_DEVICE_LOOP == 2 || key_wants_loop(key, dev_));
+            if (dloop) {
+                cudaStreamCaptureStatus cst_ = cudaStreamCaptureStatusNone;
+                cudaGraph_t g0 = nullptr;
+                dloop = cudaStreamGetCaptureInfo(cs, &cst_, nullptr, &g0) == cudaSuccess &&
+                        cudaGraphConditionalHandleCreate(&cond_h, g0, 0, 0) == cudaSuccess;   // (set by every reset)
+                if (!dloop) {
+                    cudaGetLastError();
+                    dloop_failed = true;
+                }
+            }
+            cond_on = dloop;
             spec();
+            if (dloop) capture_device_loop(cs);
+            cond_on = false;
             cudaGraph_t g = nullptr;
             const cudaError_t ce = cudaStreamEndCapture(cs, &g);
             stream = user_stream;
             if (ce != cudaSuccess) {
                 fprintf(stderr, "ksort: graph capture failed: %s\n", cudaGetErrorString(ce));
                 cudaGetLastError();
+                if (dloop) g_dloop_broken.store(1);
                 return KS_CUDA_ERROR;
             }
             cudaGraphExec_t ge = nullptr;
-            const cudaError_t ie = cudaGraphInstantiate(&ge, g, 0);
+            cudaError_t ie = dloop_failed ? cudaErrorNotSupported : cudaGraphInstantiate(&ge, g, 0);
             cudaGraphDestroy(g);
+            if (ie != cudaSuccess && dloop) {
+                // (the device loop could not be built here: this and later calls run the host loop)
+                fprintf(stderr, "ksort: device loop unavailable (%s); using the host loop\n", cudaGetErrorString(ie));
+                cudaGetLastError();
+                g_dloop_broken.store(1);
+                return fast_sort(keys, n, d_off, nseg0, ws, ws_bytes, user_stream, profile, res, h_out);
+            }
             KS_CK(ie);
             e.exec = GraphExecPtr(ge, [](cudaGraphExec_t x) { cudaGraphExecDestroy(x); });
             e.level = level;
@@ -3973,6 +4128,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             e.leaves_run = leaves_run;
             e.epoch = Q.epoch;
             e.launches = K.total();
+            e.has_loop = dloop && !dloop_failed;
             graph_store(e);
             have = true;
         }
@@ -3994,12 +4150,20 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     if (rc != KS_OK) return rc;
     // remaining work (rare): more global levels, or hand-backs queued for another leaf launch
     bool more = false;
-    while (!aborted() && (h.nseg[gcur] > 0 || h.sq_claim > 0 || h.lq_claim > 0 || h.lqb_claim > 0)) {
+    while (!aborted() && !h.done) {   // (the last reset's verdict: segments or hand-backs left)
+        // (after a replay the epoch may repeat one of the device loop's; 4096 leaf
+        // launches in one call wrap the tags' epoch field)
+        if (replayed || (Q.epoch & ((1 << kTagEpBits) - 1)) == 0) clear_ready();
         if (h.nseg[gcur] > 0) global_pass();
-        leaf();
+        leaf(hs_dev);
         more = true;
         rc = sync_status();
         if (rc != KS_OK) return rc;
+    }
+    if (more && KS_GRAPH && !profile) {
+        int dev_ = 0;
+        cudaGetDevice(&dev_);
+        key_mark_loop(GraphKey{keys, d_off, ws, n, nseg0, ws_bytes, hs_dev}, dev_);
     }
     if (more && h_out != nullptr) {
         KS_CK(cudaMemcpyAsync(h_out, keys, 8ull * n, cudaMemcpyDeviceToHost, stream));
@@ -4018,7 +4182,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             return KS_CUDA_ERROR;
         }
     }
-    res->levels = level + leaves_run;
+    res->levels = h.npasses + h.nleaves;
+    res->host_syncs = syncs;
     res->bad_index = h.bad_index == kNoIndex ? -1 : (long long)h.bad_index;
     res->mixed_zero = (h.pos_zero && h.neg_zero) ? 1 : 0;
     res->bad_arg = h.bad_arg ? 1 : 0;

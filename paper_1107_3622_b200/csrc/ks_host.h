@@ -26,6 +26,7 @@ struct FastResult {
     float phase_ms[8];
     int phase_launches[8];
     unsigned long long phase_bytes[8];
+    int host_syncs;
 };
 
 FastLayout fast_layout(long long n, long long nseg0);

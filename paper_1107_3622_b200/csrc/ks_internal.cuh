@@ -163,6 +163,9 @@ struct DevStatus {
     int pending;                      // local partitions queued or running (the only producers of leaf
                                       // items during a leaf launch; its CTAs may leave once it is zero)
     int nhb;                          // sorter hand-backs (skewed buckets), partitioned by the next leaf launch
+    int npasses, nleaves;             // global passes and leaf launches run (device-side count)
+    int published;                    // the final status went to the host (device loop: once per call)
+    int done;                         // no level left (set by the last leaf launch's reset)
     int nsmall[2];                    // small-segment lists (size classes 0, 1), sorted after the leaf launch
     int small_next[2];                // their work counters
     int nchunks;                      // chunks of the current level

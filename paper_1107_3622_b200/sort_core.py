@@ -75,6 +75,7 @@ class SortStats:
     keys_leaf_sorted: int = 0
     leaves: int = 0
     exact_used: bool = False
+    host_syncs: int = 0   # waits for the device (1: the whole recursion ran device-resident)
 
 
 last_stats = SortStats()
@@ -213,6 +214,7 @@ def _record(st: _lib.KsStatus) -> None:
     last_stats.keys_leaf_sorted = int(st.keys_leaf_sorted)
     last_stats.leaves = int(st.leaves)
     last_stats.exact_used = bool(st.exact_used)
+    last_stats.host_syncs = int(st.host_syncs)
 
 
 def _sort_device(keys: torch.Tensor, flags: int = 0) -> _lib.KsStatus:

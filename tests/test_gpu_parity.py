@@ -646,3 +646,51 @@ def test_tensor_on_non_current_device():
     with torch.cuda.device(0):
         K.k_sort(x)
     assert torch.equal(x, want)
+
+
+@pytest.mark.parametrize("kind", ["presorted", "reversed", "organ", "uniform01"])
+def test_device_resident_recursion_one_sync(kind):
+    """The reference's worklist (sort_core.py:182-198) runs on the device: once a
+    call's schedule is a cached graph, inputs needing extra global passes and
+    leaf launches (presorted, reversed, organ-pipe: the reference's adversarial
+    shapes, tests/test_sort_core.py:163-177) finish behind ONE host wait."""
+    n = 1_000_000
+    base = np.sort(O.uniform01(20260816, n))
+    if kind == "reversed":
+        base = base[::-1].copy()
+    elif kind == "organ":
+        base = np.concatenate([base[0::2], base[1::2][::-1]])
+    elif kind == "uniform01":
+        base = O.uniform01(20260816, n)
+    want = np.sort(base)
+    p = dev(base)
+    t = torch.empty_like(p)
+    for call in range(3):   # eager, capture, replay
+        t.copy_(p)
+        K.k_sort(t)
+        assert same_bits(host(t), want), (kind, call)
+        if call >= 1:
+            assert K.last_stats.host_syncs == 1, (kind, call, K.last_stats)
+    if kind != "uniform01":
+        assert K.last_stats.levels > 2, K.last_stats
+
+
+def test_device_loop_recaptured_when_a_cached_schedule_falls_short():
+    """A buffer set first sorted with uniform keys gets a graph without the
+    device loop; a presorted input on the same buffers then runs the host loop
+    once (correct output), and the next call recaptures with the loop."""
+    n = 1_000_000
+    uni = dev(O.uniform01(7, n))
+    pre = torch.sort(uni).values
+    t = torch.empty_like(uni)
+    for _ in range(3):
+        t.copy_(uni)
+        K.k_sort(t)
+        assert torch.equal(t, pre)
+    syncs = []
+    for _ in range(3):
+        t.copy_(pre)
+        K.k_sort(t)
+        assert torch.equal(t, pre)
+        syncs.append(K.last_stats.host_syncs)
+    assert syncs[-1] == 1 and syncs[-2] == 1, syncs
