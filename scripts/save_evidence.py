@@ -50,11 +50,12 @@ for r in rr[2:]:
     kern.append({"kernel": nm, "duration_us": f("gpu__time_duration.sum"), "dram_read_MB": f("dram__bytes_read.sum"),
                  "dram_write_MB": f("dram__bytes_write.sum")})
 by = {k["kernel"]: k for k in kern}
-phases = {"count": ["k_count<1>"], "scatter": ["k_scatter"], "leaf": ["k_leaf", "k_segsort<3>", "k_segsort<4>"]}
+phases = {"count": ["k_count2<1>", "k_count<1>"], "scatter": ["k_scatter2", "k_scatter"], "leaf": ["k_leaf", "k_segsort<3>", "k_segsort<4>"]}
 d = {"source": f"ncu --set full --clock-control none, C0 10M uniform01 (scripts/run_one.py), profiles/{tag}_ncu_full_summary.txt",
      "workload": "C0: 1 x 10,000,000 float64 uniform01", "kernels": kern,
-     "phases": {p: {"launches": len(v), "dram_bytes_per_launch":
-                    sum((by[k]["dram_read_MB"] + by[k]["dram_write_MB"]) * 1e6 for k in v if k in by) / len(v)}
+     "phases": {p: {"launches": len([k for k in v if k in by]), "dram_bytes_per_launch":
+                    sum((by[k]["dram_read_MB"] + by[k]["dram_write_MB"]) * 1e6 for k in v if k in by) /
+                    max(1, len([k for k in v if k in by]))}
                 for p, v in phases.items()}}
 json.dump(d, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 print(open(os.path.join(P, f"{tag}_ncu_launches.txt")).read())
