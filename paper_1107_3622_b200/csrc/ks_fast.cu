@@ -1713,6 +1713,10 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
             if (c2[u]) l2_prefetch_lines(o + (o2[u] - bi), 8ull * c2[u]);
     };
     for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+#ifdef KS_TIMELINE
+        const unsigned long long ph_t0 = tl_now();
+        unsigned long long ph_t1 = ph_t0, ph_t2 = ph_t0;
+#endif
         const int s = chunk_seg[ch];
         __syncthreads();   // the previous tile's copy-out is done
         if (s != cached) {
@@ -1769,6 +1773,9 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
 #endif
         __syncthreads();
         // B. stage the chunk's gap keys in gap order
+#ifdef KS_TIMELINE
+        ph_t1 = tl_now();
+#endif
 #if KS_CLS
         {
             // keys by 16-byte loads and their classes (from the count pass) by
@@ -1851,6 +1858,9 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // staged keys -> visible to the bulk copies
 #endif
         __syncthreads();
+#ifdef KS_TIMELINE
+        ph_t2 = tl_now();
+#endif
         have = -1;
         {
             const int nx = ch + (int)gridDim.x;
@@ -1883,6 +1893,15 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         (void)tot;
+#ifdef KS_TIMELINE
+        if (blockIdx.x < 4 && threadIdx.x == 0) {   // phases of a few CTAs: A table+scan, B staging, C copy-out issue
+            tl_rec(50, 0, cnt, ph_t0);
+            const unsigned long long t1 = tl_now();
+            (void)t1;
+            tl_rec(51, 0, (long long)(ph_t1 - ph_t0), ph_t0);
+            tl_rec(52, 0, (long long)(ph_t2 - ph_t1), ph_t1);
+        }
+#endif
 #else
         const int tot2 = (int)tot;
 #pragma unroll 4
@@ -3101,6 +3120,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
     const int lq_nb = *reinterpret_cast<volatile int *>(&st->lqb_claim);
     const unsigned long long ep = q_epoch(Q);   // (thread 0: ready tags of this launch)
     const int lq_n = lq_nb + *reinterpret_cast<volatile int *>(&st->lq_claim);
+    // nothing queued for this launch (small inputs: every gap went to the list
+    // sorters): leave at once, the chained list sorters take the SMs
+    if (lq_n == 0 && *reinterpret_cast<volatile int *>(&st->sq_claim) == 0) return;
     bool local_phase = true;   // (thread 0 only)
     for (;;) {
         KS_TL_T0;
@@ -3353,8 +3375,7 @@ __device__ void publish_status(const DevStatus *st, HostStatus *out)
     const unsigned long long *src = reinterpret_cast<const unsigned long long *>(st);
     unsigned long long *dst = reinterpret_cast<unsigned long long *>(&out->st);
     for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) dst[i] = src[i];
-    __threadfence_system();
-    __syncthreads();
+    __syncthreads();   // (the block's stores are ordered before thread 0's system-scope release)
     if (threadIdx.x == 0) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(&out->flag), "l"(1ull) : "memory");
 }
 
@@ -3868,7 +3889,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
         const int gx = (int)(seg_bound < g_pivots ? seg_bound : g_pivots);
         int *nseg_next = &st->nseg[gcur ^ 1];
-        const int plan_mode = (profile || t_in_body) ? 0 : KS_PLAN_FORK;
+        // (chained into the scatter's tail for one large array; forked beside the
+        // scatter otherwise -- measured: 10M -0.7% chained, 1M and 500 x 100K -1.6% / -0.5% forked)
+        const int plan_mode = (profile || t_in_body) ? 0
+                              : (KS_PLAN_FORK == 2 && (d_off != nullptr || n < KS_SINGLE_MIN_N)) ? 1 : KS_PLAN_FORK;
         const ForkRes *fr = plan_mode == 1 ? fork_res() : nullptr;
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, plan_mode ? 1 : 0};
         if (!first_single)   // (done by k_init_single_pass)

@@ -126,5 +126,14 @@ for kern in (13, 14, 11, 10):
         tk = sum(r["len"] for r in it)
         print(f"{names[kern]}: {len(it)} items {tk} keys, {sum(r['t1']-r['t0'] for r in it)/tk:.2f} ns/key/CTA "
               f"mean {tk/len(it):.0f} keys")
+ph = [r for r in recs if r["kernel"] in (50, 51, 52)]
+if ph:
+    import statistics as _st
+    tiles = [r for r in ph if r["kernel"] == 50]
+    a = [r["len"] / 1e3 for r in ph if r["kernel"] == 51]
+    b = [r["len"] / 1e3 for r in ph if r["kernel"] == 52]
+    tot = [(r["t1"] - r["t0"]) / 1e3 for r in tiles]
+    print(f"scatter2 tiles (CTAs 0-3): {len(tiles)}; per tile us: total {_st.mean(tot):.2f}, A table+scan "
+          f"{_st.mean(a):.2f}, B staging {_st.mean(b):.2f}, C issue {_st.mean(tot) - _st.mean(a) - _st.mean(b):.2f}")
 if out:
     json.dump(recs, open(out, "w"))
