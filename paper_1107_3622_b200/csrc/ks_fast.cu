@@ -724,30 +724,6 @@ __global__ void k_seg_offsets(Seg *segs, const int *nseg, DevStatus *st, long lo
     seg_offsets_body(segs, *nseg, st, mat_cap, ch_cap, piv_cap, lut_cap, mat, moff, tstat, nseg_next, items, sh);
 }
 
-// Single array with a level-0 global pass: status reset, routing and the pass
-// bookkeeping of k_seg_offsets in one launch.
-__global__ void k_init_single_pass(long long n, InitLists Lst, DevStatus *st, long long mat_cap, int ch_cap,
-                                   int piv_cap, int lut_cap, const unsigned *mat, const long long *moff,
-                                   unsigned long long *tstat, int items, unsigned long long magic)
-{
-    KS_PDL_ENTRY();
-    seq_advance(Lst.Q, magic);
-    KS_TL_T0;
-    __shared__ long long sh[33];
-    unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
-    for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        st->bad_index = kNoIndex;
-        st->no_item_pf = n < KS_ITEM_PF_MIN_N ? 1 : 0;
-        route_initial(0, n, Lst, st);
-    }
-    __syncthreads();
-    seg_offsets_body(Lst.gsegs, st->nseg[0], st, mat_cap, ch_cap, piv_cap, lut_cap, mat, moff, tstat, &st->nseg[1],
-                     items, sh);
-    KS_TL(20, 8, 0);
-}
-
 struct PivotsSmem {
     PivotScratch<kPMaxPow2> W;
     double piv[kPMax + kPivPad];
@@ -793,7 +769,7 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivots(Seg *segs, const int *
 // Level 0 of a single array (one segment, P up to 2047): the pivot build is on
 // the critical path while all other SMs idle, so it is spread over the GPU.
 // k_pivot_rank: each thread ranks one of the first P keys against all of them
-// (ties by position) and writes it to its sorted place; k_pivot_lut: every CTA
+// (ties by position) and writes it to its sorted place; k_front_lut: every CTA
 // de-duplicates the sorted run and builds its slice of the bucket LUT.
 constexpr int kRankThreads = 128;
 constexpr int kRankParts = 8;   // threads per ranked key (a power of two dividing 32)
@@ -836,15 +812,67 @@ __global__ void __launch_bounds__(kRankThreads) k_pivot_rank(const double *in, i
 
 constexpr int kLutCtas = 16;
 
-__global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const double *sorted, double *piv_pool,
-                                                             unsigned *lut_pool, int *chunk_seg, unsigned *mat)
+
+// Front of one large array after the pivot ranking (replaces the init kernel
+// that ran beside the ranking and the LUT kernel behind both): the last CTA
+// resets the status, advances the call sequence, routes the array, lays out
+// the level-0 pass and stores the pivots; the others build one slice each of
+// the LUT from the ranked first P keys (the single segment's P, T and table
+// offsets follow from n alone).  Both de-duplicate the ranked keys.
+__global__ void __launch_bounds__(kPivotThreads) k_front_lut(long long n, InitLists Lst, DevStatus *st, long long mat_cap,
+                                                             int ch_cap, int piv_cap, int lut_cap, unsigned *mat,
+                                                             const long long *moff, unsigned long long *tstat, int items,
+                                                             unsigned long long magic, const double *sorted,
+                                                             double *piv_pool, unsigned *lut_pool, int *chunk_seg)
 {
     KS_PDL_ENTRY();
     KS_TL_T0;
     __shared__ double piv[kPMax + kPivPad];
     __shared__ long long sh[33];
-    const Seg g = segs[0];
-    const int P = g.P;
+    const bool init_cta = blockIdx.x == gridDim.x - 1;
+    if (init_cta) {
+        seq_advance(Lst.Q, magic);
+        unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
+        for (int i = threadIdx.x; i < (int)(sizeof(DevStatus) / 8); i += blockDim.x) w[i] = 0ull;
+        __syncthreads();
+        __shared__ long long s_nt;
+        if (threadIdx.x == 0) {
+            // route_initial + seg_offsets_body for the one segment (no block scans)
+            st->bad_index = kNoIndex;
+            st->no_item_pf = n < KS_ITEM_PF_MIN_N ? 1 : 0;
+            long long chunk = cdiv(cdiv(n, (long long)min(items, kChunkItemsMax)), (long long)kChunkAlign) * kChunkAlign;
+            if (KS_STAGED && chunk > kStageMax) chunk = kStageMax;
+            if (chunk < kChunkMin) chunk = kChunkMin;
+            Seg g = make_seg(0, n, 0);
+            g.P = pivots_for(n, kPMax);
+            g.rows = 2 * g.P + 1;
+            g.nch = (int)cdiv(n, chunk);
+            g.T = lut_for(g.P, kLutMax);
+            g.piv_off = g.lut_off = g.ch_off = 0;
+            g.mat_off = 0;
+            Lst.gsegs[0] = g;
+            st->nseg[0] = 1;
+            st->nseg[1] = 0;
+            ++st->npasses;
+            const long long c_mat = mat_entries(g);
+            st->nchunks = g.nch;
+            st->chunk = (int)chunk;
+            st->mat_total = c_mat;
+            add_bytes(st, kPhScan, 16ull * (unsigned long long)c_mat);
+            add_bytes(st, kPhPivots, 8ull * (unsigned long long)(g.P + 1));
+            if (c_mat > mat_cap || g.nch > ch_cap || g.P + 1 > piv_cap || g.T > lut_cap || Lst.seg_cap < 1) {
+                st->overflow = 2;
+                st->nchunks = 0;
+                st->mat_total = 0;
+            }
+            st->scan_next = 0;
+            s_nt = c_mat <= mat_cap ? cdiv(c_mat, (long long)kScanBlock) : 0;
+        }
+        __syncthreads();
+        for (long long i = threadIdx.x; i < s_nt; i += blockDim.x) tstat[i] = 0ull;   // look-back words
+        __syncthreads();
+    }
+    const int P = pivots_for(n, kPMax);
     long long carry = 0;
     for (int base = 0; base < P; base += blockDim.x) {
         const int i = base + threadIdx.x;
@@ -858,14 +886,13 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
     const int k = (int)carry;
     if (threadIdx.x < kPivPad) piv[k + threadIdx.x] = CUDART_NAN;
     __syncthreads();
-    // same transform as build_pivots
-    int T = g.T;
+    int T = lut_for(P, kLutMax);   // (= the layout's g.T; the single segment's LUT and pivots start at 0)
     const double lo = piv[0];
     double scale;
     lut_transform(piv, k, T, scale);
-    // this CTA's LUT slice: one bucket run per thread, a = #pivots in buckets < t
-    const int per_cta = (T + gridDim.x - 1) / gridDim.x;
-    const int c0 = blockIdx.x * per_cta, c1 = min(T, c0 + per_cta);
+    const int nlut = gridDim.x - 1;
+    const int per_cta = (T + nlut - 1) / nlut;
+    const int c0 = blockIdx.x * per_cta, c1 = init_cta ? c0 : min(T, c0 + per_cta);
     const int per = (c1 - c0 + (int)blockDim.x - 1) / (int)blockDim.x;
     const int t0 = c0 + threadIdx.x * per, t1 = min(c1, t0 + per);
     if (t0 < t1) {
@@ -877,14 +904,17 @@ __global__ void __launch_bounds__(kPivotThreads) k_pivot_lut(Seg *segs, const do
         for (int t = t0; t < t1; ++t) {
             int b = a;
             while (b < k && lut_bucket(piv[b], lo, scale, T) <= t) ++b;
-            lut_pool[g.lut_off + t] = lut_pack(a, b);
+            lut_pool[t] = lut_pack(a, b);
             a = b;
         }
     }
-    if (blockIdx.x == 0) {
+    if (init_cta) {
+        Seg *segs = Lst.gsegs;
+        const Seg g = segs[0];
         for (int i = threadIdx.x; i <= k; i += blockDim.x) piv_pool[g.piv_off + i] = piv[i];
         for (int c = threadIdx.x; c < g.nch; c += blockDim.x) chunk_seg[g.ch_off + c] = 0;
         for (int q = threadIdx.x; q <= g.P; q += blockDim.x) mat[mat_eq(g, q)] = 0u;   // equality-run totals
+        __syncthreads();
         if (threadIdx.x == 0) {
             segs[0].k = k;
             segs[0].T = T;
@@ -3839,23 +3869,16 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         }
         if (d_off == nullptr) {
             if (n > kInitLocalMax) {   // (+ the level-0 pass bookkeeping)
-                // the level-0 pivot ranking needs only the input: forked next to the init kernel
-                const ForkRes *fr = (KS_PLAN_FORK && !profile) ? fork_res() : nullptr;
-                if (fr != nullptr) {
-                    cudaEventRecord(fr->fork, stream);
-                    cudaStreamWaitEvent(fr->side, fr->fork, 0);
-                    launch_rank(fr->side);
-                }
-                K.run(kPhGate, [&] {
-                    launch(k_init_single_pass, dim3(1), dim3(1024), 0, stream, n, Lst, st, L.mat_cap, L.ch_cap,
-                           L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum),
-                           pass_items, ws_magic);
+                // the first P keys ranked, then one launch for the init, the level-0
+                // layout and the pivot LUT (PDL: its CTAs wait at griddepcontrol.wait)
+                launch_rank(stream);
+                K.run(kPhPivots, [&] {
+                    launch(k_front_lut, dim3(kLutCtas + 1), dim3(kPivotThreads), 0, stream, n, Lst, st, L.mat_cap, L.ch_cap,
+                           L.piv_cap, L.lut_cap, mat, (const long long *)moff,
+                           reinterpret_cast<unsigned long long *>(bsum), pass_items, ws_magic,
+                           (const double *)reinterpret_cast<double *>(moff), piv, lut, chunk_seg);
                 });
-                if (fr != nullptr) {
-                    cudaEventRecord(fr->join, fr->side);
-                    cudaStreamWaitEvent(stream, fr->join, 0);
-                    rank_done = true;
-                }
+                rank_done = true;
             } else
                 K.run(kPhGate, [&] { launch(k_init_single, dim3(1), dim3(64), 0, stream, n, Lst, st, ws_magic); });
             if (n <= kInitLocalMax)
@@ -3883,7 +3906,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const int dst_id = (level & 1) ? 0 : 1;
         int *nseg_cur = &st->nseg[gcur];
         // segments at this level: known on the host at level 0, else bounded by the table size
-        // (level 0 of one large array: its layout comes from k_init_single_pass; a
+        // (level 0 of one large array: its layout comes from k_front_lut; a
         // small array's first pass -- only ever the device loop's no-op -- is generic)
         const bool first_single = level == 0 && d_off == nullptr && n > kInitLocalMax;
         const long long seg_bound = level == 0 ? (d_off == nullptr ? 1 : nseg0) : L.seg_cap;
@@ -3895,19 +3918,13 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
                               : (KS_PLAN_FORK == 2 && (d_off != nullptr || n < KS_SINGLE_MIN_N)) ? 1 : KS_PLAN_FORK;
         const ForkRes *fr = plan_mode == 1 ? fork_res() : nullptr;
         EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, plan_mode ? 1 : 0};
-        if (!first_single)   // (done by k_init_single_pass)
+        if (!first_single)   // (done by k_front_lut)
             K.run(kPhPivots, [&] {
                 launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
                        L.piv_cap, L.lut_cap, mat, moff, reinterpret_cast<unsigned long long *>(bsum), nseg_next,
                        pass_items);
             });
-        if (first_single) {   // one segment, known P: build the pivots GPU-wide
-            double *sorted = reinterpret_cast<double *>(moff);   // (scratch: the offsets are written later)
-            if (!rank_done) launch_rank(stream);
-            K.run(kPhPivots, [&] {
-                launch(k_pivot_lut, dim3(kLutCtas), dim3(kPivotThreads), 0, stream, segs[gcur], sorted, piv, lut,
-                       chunk_seg, mat);
-            });
+        if (first_single) {   // one segment, known P: pivots and LUT built by k_front_lut
         } else {
             K.run(kPhPivots, [&] {
                 launch(k_pivots, dim3(gx), dim3(kPivotThreads), sizeof(PivotsSmem), stream, segs[gcur], nseg_cur, src,
