@@ -2450,7 +2450,12 @@ __device__ void finish_item(const Item &it, double *keys, const double *tmp, dou
 //      depend on the value distribution
 //   4. coalesced write-back.
 // ---------------------------------------------------------------------------
-constexpr int kMidCap = 256;   // listed 5..kThreadSortMax-key buckets (single buffer); beyond: the owner sorts
+constexpr int kMidCap = 384;   // listed 5..kThreadSortMax-key buckets (single buffer); beyond: the owner sorts
+constexpr int kMid16Cap = 32;  // ... of them for 9..16-key buckets (rare: Poisson(2) puts 0.02% of buckets there)
+#ifndef KS_MID_NET
+#define KS_MID_NET 28  // bit c: size class c sorts its 5..8-key buckets with one thread each and an 8-key
+#endif                 // network (else a half-warp's ranks). Classes 2, 3, 4 -- the throughput-bound sorters:
+                       // C0 -2%, C4 -3.6%; classes 0 / 1 serve latency-bound small calls: C1 +5% with it
 template <int C>
 struct SortSmem {
     static constexpr int kT = sort_threads(C), kCap = sort_cap(C), kLam = sort_lambda(C);
@@ -2472,7 +2477,8 @@ struct SortSmem {
     int bits;              // bucket map in the order-preserving bit image (wide segments)
     unsigned sh[33];
     int nbig;
-    int nmid;              // buckets of 5..kThreadSortMax keys (listed in the free `a` buffer)
+    int nmid;              // buckets of 5..8 keys (listed in the free `a` buffer)
+    int nmid16;            // buckets of 9..kThreadSortMax keys (listed behind them)
     int nhb;               // hand-back buckets (published once the segment is written)
     int hb[kCap / (kUnitMax + 1) + 1];
     int mid[kSingle ? kMidCap : 1];   // (single buffer: no free `a` for the list)
@@ -2853,7 +2859,14 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         //     stored straight to the final place; 5..kThreadSortMax keys ->
         //     listed (the `a` buffer is free now) for 4b
         int *mid = Smem::kSingle ? S.mid : reinterpret_cast<int *>(S.a);
-        if (tid == 0) S.nmid = 0;
+        // 5..8-key buckets from the front, 9..16 behind them (KS_MID_NET; else one list)
+        constexpr bool kNet = ((KS_MID_NET >> C) & 1) != 0;
+        constexpr int kMid8Cap = (Smem::kSingle ? kMidCap : 2 * Smem::kA) - (kNet ? kMid16Cap : 0);
+        int *mid16 = mid + kMid8Cap;
+        if (tid == 0) {
+            S.nmid = 0;
+            S.nmid16 = 0;
+        }
         __syncthreads();
 #pragma unroll 1
         for (int b0 = tid; b0 < B; b0 += 2 * kT) {   // two buckets in flight per thread
@@ -2865,9 +2878,10 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 const int sz = (int)S.cur[b] - s0;
                 if (sz == 0 || sz > kThreadSortMax) continue;
                 if (sz > 4) {
-                    const int q = atomicAdd(&S.nmid, 1);
-                    if (!Smem::kSingle || q < kMidCap) {
-                        mid[q] = b;
+                    const bool big16 = kNet && sz > 8;
+                    const int q = atomicAdd(big16 ? &S.nmid16 : &S.nmid, 1);
+                    if (q < (big16 ? kMid16Cap : kMid8Cap)) {
+                        (big16 ? mid16 : mid)[q] = b;
                     } else {   // list full: the owner sorts it
                         smem_insertion_sort(bb + s0, sz);
                         if (!KS_SEG_TMA)
@@ -2894,7 +2908,40 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         // 4b. 5..kThreadSortMax keys: a half-warp per bucket, lane l takes key l
         //     to its rank in the bucket (ties by position) -- no serial chain
         //     (was: one thread per bucket, insertion sort; 0.377 -> 0.368 ms at C0)
-        const int nmid = Smem::kSingle ? min(S.nmid, kMidCap) : S.nmid;
+        int nmid;
+        if constexpr (kNet) {
+            // 4b. 5..8 keys: one thread per bucket, 19-comparator 8-key network in
+            //     registers (+inf padding), in place; the rare 9..16-key buckets by
+            //     half-warp ranks below (a half-warp per 5..8-key bucket left most
+            //     lanes idle: 20% of the sorter's warp instructions for 15% of the keys)
+            {
+                const int n8 = min(S.nmid, kMid8Cap);
+    #pragma unroll 1
+                for (int q = tid; q < n8; q += kT) {
+                    const int b = mid[q];
+                    const int s0 = b ? (int)S.cur[b - 1] : 0;
+                    const int sz = (int)S.cur[b] - s0;
+                    double *x = bb + s0;
+                    double v[8];
+    #pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = i < sz ? x[i] : CUDART_INF;
+                    cas(v[0], v[2], true); cas(v[1], v[3], true); cas(v[4], v[6], true); cas(v[5], v[7], true);
+                    cas(v[0], v[4], true); cas(v[1], v[5], true); cas(v[2], v[6], true); cas(v[3], v[7], true);
+                    cas(v[0], v[1], true); cas(v[2], v[3], true); cas(v[4], v[5], true); cas(v[6], v[7], true);
+                    cas(v[2], v[4], true); cas(v[3], v[5], true);
+                    cas(v[1], v[4], true); cas(v[3], v[6], true);
+                    cas(v[1], v[2], true); cas(v[3], v[4], true); cas(v[5], v[6], true);
+                    double *o = KS_SEG_TMA ? x : out + s0;
+    #pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        if (i < sz) o[i] = v[i];
+                }
+            }
+            nmid = min(S.nmid16, kMid16Cap);
+            mid = mid16;
+        } else {
+            nmid = Smem::kSingle ? min(S.nmid, kMid8Cap) : S.nmid;
+        }
 #if KS_MID_RANK
         static_assert(kThreadSortMax <= 16, "one half-warp lane per key");
 #if KS_SEG_TMA
