@@ -152,7 +152,7 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #define KS_MINB3 3
 #endif
 #ifndef KS_SINGLE2
-#define KS_SINGLE2 0      // the leaf's class-2 sorter with a single shared buffer (room for larger segments)
+#define KS_SINGLE2 1      // the leaf's class-2 sorter with a single shared buffer (room for 20K-key segments)
 #endif
 #ifndef KS_PLAN_FORK
 #define KS_PLAN_FORK 2    // the global plan runs concurrently with the scatter (data writes deferred to the finish
