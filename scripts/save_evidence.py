@@ -22,9 +22,9 @@ hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hi]
 I = {x: i for i, x in enumerate(h)}
 ks = [r for r in rows[hi + 1:] if len(r) == len(h) and r[I["Metric Name"]] == "gpu__time_duration.sum"]
-idx = [i for i, r in enumerate(ks) if "k_init" in r[I["Kernel Name"]]]
-if idx[-1] > 0 and "k_pivot_rank" in ks[idx[-1] - 1][I["Kernel Name"]]:
-    idx[-1] -= 1   # (the level-0 ranking is forked next to the init kernel and launched first)
+# a step starts with the level-0 pivot ranking (round 2) or the init kernel (round 1 builds)
+idx = [i for i, r in enumerate(ks) if "k_pivot_rank" in r[I["Kernel Name"]]] or \
+      [i for i, r in enumerate(ks) if "k_init" in r[I["Kernel Name"]]]
 with open(os.path.join(P, f"{tag}_ncu_launches.txt"), "w") as fh:
     fh.write("# ncu launch list (gpu__time_duration.sum, --clock-control none) of the last timed bench step, "
              "C0 10M uniform01 (serialised by ncu; the side-stream launches run concurrently in the bench)\n")
