@@ -29,12 +29,17 @@ with open(os.path.join(P, f"{tag}_ncu_launches.txt"), "w") as fh:
     fh.write("# ncu launch list (gpu__time_duration.sum, --clock-control none) of the last timed bench step, "
              "C0 10M uniform01 (serialised by ncu; the side-stream launches run concurrently in the bench)\n")
     tot = 0.0
-    for r in ks[idx[-1]:]:
+    step = []
+    for r in ks[idx[-1]:]:   # (until the first kernel that is not the engine's: the bench's context timings)
+        if step and "k_" not in r[I["Kernel Name"]]:
+            break
+        step.append(r)
+    for r in step:
         nm = r[I["Kernel Name"]].split("(")[0].replace("void ", "")
         t = float(r[I["Metric Value"]].replace(",", "")) / 1000.0
         tot += t
         fh.write("%-40s %8.1f us\n" % (nm, t))
-    fh.write("%-40s %8.1f us over %d launches\n" % ("total", tot, len(ks) - idx[-1]))
+    fh.write("%-40s %8.1f us over %d launches\n" % ("total", tot, len(step)))
 # DRAM traffic per launch from the full capture (first occurrence of each kernel)
 raw = subprocess.run(["ncu", "-i", os.path.join(G, f"full_{tag}.ncu-rep"), "--page", "raw", "--csv"],
                      capture_output=True, text=True).stdout
