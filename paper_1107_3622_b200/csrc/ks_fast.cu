@@ -178,6 +178,9 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #ifndef KS_DEVICE_LOOP
 #define KS_DEVICE_LOOP 1   // graph path: the remaining levels run in a conditional WHILE node (no host round
 #endif                     // trip) -- 1: for keys whose sorts needed it before, 2: always, 0: never
+#ifndef KS_DRAIN0
+#define KS_DRAIN0 1       // one large array: the class-1 list sorters drain the class-0 list in the same launch
+#endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
 #endif
@@ -3053,7 +3056,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
 template <int C>
 __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ? KS_MINB3 : (C == 4 ? KS_MINB4 : KS_MINB1)))
     k_segsort(const Seg *list, const int *count, int *next, LeafQ Q, DevStatus *st, double *keys, const double *tmp,
-              const Item *units, int chained)
+              const Item *units, int chained, const Seg *list0, const int *count0, int *next0, int drain0)
 {
     // chained: launched programmatically behind the leaf kernel (or behind the
     // other list sorter) and started on the SMs its CTAs leave.  The lists are
@@ -3076,68 +3079,53 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         if (chained) asm volatile("griddepcontrol.wait;" ::: "memory");
         return;
     }
-    const int n = *count;
     unsigned long long keys_sorted = 0, segs_sorted = 0;
     // thread 0 claims one item ahead and pulls its input and output ranges into
     // L2 while the current one is sorted (a cold segment otherwise costs two
     // DRAM round trips to load and a fill stall per partially written sector)
     const bool pf = !st->no_item_pf;
-    auto prefetch = [&](int d) {
-#if KS_PREFETCH
-        if (d < n && pf) {
-            const Seg g = list[d];
-            l2_prefetch((g.src ? tmp : keys) + g.start, 8ull * g.len);
-            if (g.src) l2_prefetch(keys + g.start, 8ull * g.len);
-        }
-#endif
-    };
-#if KS_SEG_FEED
-    // descriptors of the current and the next item in shared memory (see SegFeed)
     __shared__ __align__(16) Seg s_seg[2];
     __shared__ int s_idx[2];
     (void)s_item;
-    if (threadIdx.x == 0) {
-        const int d = atomicAdd(next, 1);
-        s_idx[0] = d;
-        if (d < n) {
-            s_seg[0] = list[d];
-            prefetch(d);
-        }
-    }
-    for (int slot = 0;; slot ^= 1) {
-        __syncthreads();
-        if (s_idx[slot] >= n) break;
-        const Seg g = s_seg[slot];
-        SegFeed f{list, n, 0, &s_seg[slot ^ 1], &s_idx[slot ^ 1], keys, tmp, false, pf};
-        if (threadIdx.x == 0) f.d = atomicAdd(next, 1);   // (used after the load phase)
-        KS_TL_T0;
-        segsort_one<C>(S, g, Q, st, keys, tmp, f);
-        f.after_scatter();   // (no-op unless the segment took no scatter path)
-        KS_TL(10 + C, 1, g.len);
-        keys_sorted += (unsigned long long)g.len;
-        segs_sorted += 1;
-    }
-#else
-    if (threadIdx.x == 0) {
-        s_item = atomicAdd(next, 1);
-        prefetch(s_item);
-    }
-    for (;;) {
-        __syncthreads();
-        const int d = s_item;
-        if (d >= n) break;
-        const Seg g = list[d];
-        __syncthreads();   // everyone has read s_item
-        if (threadIdx.x == 0) {
-            s_item = atomicAdd(next, 1);
-            prefetch(s_item);
-        }
-        segsort_one<C>(S, g, Q, st, keys, tmp);
-        keys_sorted += (unsigned long long)g.len;
-        segs_sorted += 1;
-        __syncthreads();
-    }
+    auto run_list = [&](const Seg *lst, int n, int *nxt) {
+        auto prefetch = [&](int d) {
+#if KS_PREFETCH
+            if (d < n && pf) {
+                const Seg g = lst[d];
+                l2_prefetch((g.src ? tmp : keys) + g.start, 8ull * g.len);
+                if (g.src) l2_prefetch(keys + g.start, 8ull * g.len);
+            }
 #endif
+        };
+        // descriptors of the current and the next item in shared memory (see SegFeed)
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int d = atomicAdd(nxt, 1);
+            s_idx[0] = d;
+            if (d < n) {
+                s_seg[0] = lst[d];
+                prefetch(d);
+            }
+        }
+        for (int slot = 0;; slot ^= 1) {
+            __syncthreads();
+            if (s_idx[slot] >= n) break;
+            const Seg g = s_seg[slot];
+            SegFeed f{lst, n, 0, &s_seg[slot ^ 1], &s_idx[slot ^ 1], keys, tmp, false, pf};
+            if (threadIdx.x == 0) f.d = atomicAdd(nxt, 1);   // (used after the load phase)
+            KS_TL_T0;
+            segsort_one<C>(S, g, Q, st, keys, tmp, f);
+            f.after_scatter();   // (no-op unless the segment took no scatter path)
+            KS_TL(10 + C, 1, g.len);
+            keys_sorted += (unsigned long long)g.len;
+            segs_sorted += 1;
+        }
+    };
+    run_list(list, *count, next);
+    // one large array: the class-0 list after the class-1 list in the same
+    // launch (it fills the class-1 sorters' tail; as a kernel of its own behind
+    // them it was the sort's last 30 us for 3 us of work)
+    if (drain0) run_list(list0, *count0, next0);
 #if KS_SEG_TMA
     if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");   // (S reused / freed next)
 #endif
@@ -3147,12 +3135,11 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         atomicAdd(&st->leaves, segs_sorted);
     }
     KS_TL(10 + C, 8, keys_sorted);
-    if (C == 0 || C == 4) {   // the last kernel of the launch also finishes the warp units and fills
+    if (C == 0 || C == 4 || drain0) {   // the last kernel of the launch also finishes the warp units and fills
         constexpr int kW = sort_threads(C) / 32;
-        static_assert((C != 0 && C != 4) || kW * sidx_size(kUnitMax) <= SortSmem<C>::kA + SortSmem<C>::kCap,
-                      "unit scratch fits a + b");
+        static_assert(kW * sidx_size(kUnitMax) <= SortSmem<C>::kA + SortSmem<C>::kCap, "unit scratch fits a + b");
         __syncthreads();
-        double *sm = S.a + (threadIdx.x >> 5) * sidx_size(kUnitMax);   // (a and b are contiguous)
+        double *sm = (SortSmem<C>::kA > 1 ? S.a : S.b) + (threadIdx.x >> 5) * sidx_size(kUnitMax);   // (a, b contiguous)
         const int nu = st->nunits;
         for (int d = blockIdx.x * kW + (threadIdx.x >> 5); d < nu; d += gridDim.x * kW) finish_item(units[d], keys, tmp, sm);
     }
@@ -4071,25 +4058,32 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
             s0 = fr->side;
         }
         const int ch1 = chain ? 1 : 0, ch0 = (chain && s0 == stream) ? 1 : 0;
+        // one large array: the class-1 sorters also drain the class-0 list (and finish the units)
+        const int drain0 = (KS_DRAIN0 && n >= KS_SINGLE_MIN_N && fr == nullptr) ? 1 : 0;
         if (n >= KS_SINGLE_MIN_N)
             K.run(kPhLeaf, [&] {
                 launch_pdl(chain, k_segsort<3>, dim3(cfg->g_small3), dim3(sort_threads(3)), sort_smem<3>(), stream,
-                           Q.small[1], &st->nsmall[1], &st->small_next[1], Q, st, keys, tmp, units, ch1);
+                           Q.small[1], &st->nsmall[1], &st->small_next[1], Q, st, keys, tmp, units, ch1,
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], drain0);
             });
         else
             K.run(kPhLeaf, [&] {
                 launch_pdl(chain, k_segsort<1>, dim3(cfg->g_small[1]), dim3(sort_threads(1)), sort_smem<1>(), stream,
-                           Q.small[1], &st->nsmall[1], &st->small_next[1], Q, st, keys, tmp, units, ch1);
+                           Q.small[1], &st->nsmall[1], &st->small_next[1], Q, st, keys, tmp, units, ch1,
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], 0);
             });
-        if (n >= KS_SINGLE_MIN_N)   // (same trade-off for the class-0 list: 8 single-buffer sorters per SM)
+        if (drain0) {
+        } else if (n >= KS_SINGLE_MIN_N)   // (same trade-off for the class-0 list: 8 single-buffer sorters per SM)
             K.run(kPhLeaf, [&] {
                 launch_pdl(ch0 != 0, k_segsort<4>, dim3(cfg->g_small4), dim3(sort_threads(4)), sort_smem<4>(), s0,
-                           Q.small[0], &st->nsmall[0], &st->small_next[0], Q, st, keys, tmp, units, ch0);
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], Q, st, keys, tmp, units, ch0,
+                           (const Seg *)nullptr, (const int *)nullptr, (int *)nullptr, 0);
             });
         else
             K.run(kPhLeaf, [&] {
                 launch_pdl(ch0 != 0, k_segsort<0>, dim3(cfg->g_small[0]), dim3(sort_threads(0)), sort_smem<0>(), s0,
-                           Q.small[0], &st->nsmall[0], &st->small_next[0], Q, st, keys, tmp, units, ch0);
+                           Q.small[0], &st->nsmall[0], &st->small_next[0], Q, st, keys, tmp, units, ch0,
+                           (const Seg *)nullptr, (const int *)nullptr, (int *)nullptr, 0);
             });
         if (fr != nullptr) {
             cudaEventRecord(fr->join, fr->side);
