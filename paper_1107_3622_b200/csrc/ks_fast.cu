@@ -181,6 +181,9 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #ifndef KS_DRAIN0
 #define KS_DRAIN0 1       // one large array: the class-1 list sorters drain the class-0 list in the same launch
 #endif
+#ifndef KS_LU1024
+#define KS_LU1024 8       // segment sorter loads in flight per thread at 1024 threads (the leaf kernel's class 2; 4: C0 +0.8%)
+#endif
 #ifndef KS_PASS_MINB
 #define KS_PASS_MINB 3    // min resident CTAs per SM requested for count / scatter
 #endif
@@ -2454,6 +2457,8 @@ __device__ void finish_item(const Item &it, double *keys, const double *tmp, dou
 //   4. coalesced write-back.
 // ---------------------------------------------------------------------------
 constexpr int kMidCap = 384;   // listed 5..kThreadSortMax-key buckets (single buffer); beyond: the owner sorts
+// (5.3% of the B = len/2 buckets hold 5..16 keys: the leaf's 20K-key class needs ~540 entries)
+__host__ __device__ constexpr int mid_cap(int c) { return c == 2 ? 1536 : kMidCap; }
 constexpr int kMid16Cap = 32;  // ... of them for 9..16-key buckets (rare: Poisson(2) puts 0.02% of buckets there)
 #ifndef KS_MID_NET
 #define KS_MID_NET 28  // bit c: size class c sorts its 5..8-key buckets with one thread each and an 8-key
@@ -2484,7 +2489,7 @@ struct SortSmem {
     int nmid16;            // buckets of 9..kThreadSortMax keys (listed behind them)
     int nhb;               // hand-back buckets (published once the segment is written)
     int hb[kCap / (kUnitMax + 1) + 1];
-    int mid[kSingle ? kMidCap : 1];   // (single buffer: no free `a` for the list)
+    int mid[kSingle ? mid_cap(C) : 1];   // (single buffer: no free `a` for the list)
 };
 
 // f(i, key) for every key of in[0, m), kLU loads in flight per thread (L2 only)
@@ -2658,7 +2663,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     double *const bb = S.b + (KS_SEG_TMA ? (int)(start & 1) : 0);
     const double *in = (g.src ? tmp : keys) + start;
     double *out = keys + start;
-    constexpr int kLU = kT >= 1024 ? 4 : 8;   // loads in flight per thread (one round trip for most segments)
+    constexpr int kLU = kT >= 1024 ? KS_LU1024 : 8;   // loads in flight per thread (one round trip for most segments)
     int B = m / Smem::kLam;
     B = B < 1 ? 1 : (B > Smem::kBuckets ? Smem::kBuckets : B);
     // Bounded item (its keys lie between two of the parent's pivots): the
@@ -2864,7 +2869,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         int *mid = Smem::kSingle ? S.mid : reinterpret_cast<int *>(S.a);
         // 5..8-key buckets from the front, 9..16 behind them (KS_MID_NET; else one list)
         constexpr bool kNet = ((KS_MID_NET >> C) & 1) != 0;
-        constexpr int kMid8Cap = (Smem::kSingle ? kMidCap : 2 * Smem::kA) - (kNet ? kMid16Cap : 0);
+        constexpr int kMid8Cap = (Smem::kSingle ? mid_cap(C) : 2 * Smem::kA) - (kNet ? kMid16Cap : 0);
         int *mid16 = mid + kMid8Cap;
         if (tid == 0) {
             S.nmid = 0;
