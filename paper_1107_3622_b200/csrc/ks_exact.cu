@@ -41,7 +41,7 @@ struct XStatus {
     int nsmall;
     int nlog;
     int overflow;
-    int pad;
+    int levels;   // levels that had work (counted on the device: the host launches them in batches)
     unsigned long long comparisons, moves;
 };
 
@@ -305,6 +305,22 @@ __global__ void k_exact_small(const XSeg *small, const int *nsmall, const double
     if (mv) atomicAdd(&xs->moves, mv);
 }
 
+// level bookkeeping on the device (the host launches kExactBatch levels per
+// status read): phase 0, after the small-segment kernel: count the level,
+// empty the small list and the next big table; phase 1, after the level
+// kernel: the next table becomes the current one.
+__global__ void k_exact_advance(XStatus *xs, int phase)
+{
+    if (threadIdx.x || blockIdx.x) return;
+    if (phase == 0) {
+        if (xs->nsmall > 0 || xs->nbig[0] > 0) ++xs->levels;
+        xs->nsmall = 0;
+        xs->nbig[1] = 0;
+    } else {
+        xs->nbig[0] = xs->nbig[1];
+    }
+}
+
 __global__ void k_exact_init(long long n, XSeg *big, XSeg *small, XStatus *xs)
 {
     if (threadIdx.x || blockIdx.x) return;
@@ -444,34 +460,36 @@ int exact_sort(double *keys, long long n, void *ws, size_t ws_bytes, cudaStream_
 
     // xs->nbig[0] counts the current level's big segments (table big[cur]);
     // k_exact_level appends the next level's to big[cur ^ 1] through nbig[1].
+    // Levels are launched in batches with fixed grids (the kernels read their
+    // segment counts on the device and exit at once when a level is empty):
+    // one status read per kExactBatch levels instead of one per level.
+    constexpr int kExactBatch = 16;
     int level = 0;
     int cur = 0;
+    int syncs = 1;
     while (h.nbig[0] > 0 || h.nsmall > 0) {
-        const double *src = (level & 1) ? tmp : keys;
-        double *dst = (level & 1) ? keys : tmp;
-        // small segments of this level live in `src` (they were produced by the previous level)
-        if (h.nsmall > 0) {
-            k_exact_small<<<cdiv(h.nsmall, 128), 128, 0, stream>>>(small, &xs->nsmall, src, keys,
-                                                                   (level & 1) ? 0 : 1, xs, log, L.log_cap);
-            XK_CK(cudaMemsetAsync(&xs->nsmall, 0, sizeof(int), stream));
-        }
-        if (h.nbig[0] > 0) {
-            XK_CK(cudaMemsetAsync(&xs->nbig[1], 0, sizeof(int), stream));
-            int grid = h.nbig[0] < sms * 2 ? h.nbig[0] : sms * 2;
-            k_exact_level<<<grid, kExactThreads, 0, stream>>>(big[cur], &xs->nbig[0], src, dst, keys,
-                                                              (level & 1) ? 1 : 0, Bl, Gl, big[cur ^ 1], small,
-                                                              xs, log, L.log_cap, L.big_cap, L.small_cap);
-            XK_CK(cudaMemcpyAsync(&xs->nbig[0], &xs->nbig[1], sizeof(int), cudaMemcpyDeviceToDevice, stream));
+        for (int b = 0; b < kExactBatch; ++b) {
+            const double *src = (level & 1) ? tmp : keys;
+            double *dst = (level & 1) ? keys : tmp;
+            // small segments of this level live in `src` (they were produced by the previous level)
+            k_exact_small<<<sms * 4, 128, 0, stream>>>(small, &xs->nsmall, src, keys, (level & 1) ? 0 : 1, xs, log,
+                                                       L.log_cap);
+            k_exact_advance<<<1, 32, 0, stream>>>(xs, 0);
+            k_exact_level<<<sms * 2, kExactThreads, 0, stream>>>(big[cur], &xs->nbig[0], src, dst, keys,
+                                                                 (level & 1) ? 1 : 0, Bl, Gl, big[cur ^ 1], small, xs,
+                                                                 log, L.log_cap, L.big_cap, L.small_cap);
+            k_exact_advance<<<1, 32, 0, stream>>>(xs, 1);
             cur ^= 1;
-        } else {
-            XK_CK(cudaMemsetAsync(&xs->nbig[0], 0, sizeof(int), stream));
+            ++level;
         }
         XK_CK(cudaGetLastError());
         XK_CK(cudaMemcpyAsync(&h, xs, sizeof(XStatus), cudaMemcpyDeviceToHost, stream));
         XK_CK(cudaStreamSynchronize(stream));
+        ++syncs;
         if (h.overflow) return KS_CUDA_ERROR;
-        ++level;
     }
+    (void)syncs;
+    level = h.levels;
     res->levels = level;
     res->comparisons = h.comparisons;
     res->moves = h.moves;

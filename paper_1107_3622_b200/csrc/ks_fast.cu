@@ -1980,6 +1980,10 @@ struct EmitArgs {
     int in_leaf;       // emitting inside the leaf launch: local children go to the sort queue
     int defer;         // running concurrently with the scatter: no reads of the scattered data and no
                        // writes to the scatter's source -- tiny gaps become units, pivot runs fill items
+    int merge_cand;    // merging (see emit_pairs): pairs up to this many keys are candidates,
+    int merge_t;       // ... grouped by floor(run prefix / merge_t); 0: kMergeCand / kMergeT
+    int to_leaf;       // one small array: every segment of kUnitMax < len <= kSortMax keys goes to the
+                       // leaf kernel's sort queue (one ~n/SMs-key group per SM, one wave) instead of the lists
 };
 
 // packed per-thread counts for one block scan (11 bits each; blocks <= 1024 threads):
@@ -2078,17 +2082,20 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
 {
     const int stall = 4 * gl > 3 * plen ? 1 : 0;   // this gap kept > 3/4 of the parent's keys
     int u_gap = 0, s_gap = 0, l_gap = 0, g_gap = 0, t_gap = 0;
+    long long s_ag = ag, s_gl = gl;   // the sort-queue item of this thread (its gap, or the merged group it closes)
+    double s_blo = blo;
     bool merged = false;
 #if KS_MERGE
     if (KS_MERGE == 2 || !A.in_leaf) {   // (block-uniform; in the leaf it costs more than it saves)
         const long long sz = gl + el;
-        const bool cand = have && sz <= kMergeCand && el <= kFillDirect;
+        const int mcand = A.merge_t > 0 ? A.merge_cand : kMergeCand, mt = A.merge_t > 0 ? A.merge_t : kMergeT;
+        const bool cand = have && sz <= mcand && el <= kFillDirect;
         const long long x = block_exclusive_scan(cand ? sz : 0, sh, nullptr);   // (non-candidates add 0)
         const bool prev_cand = mg_prev_cand(mg, cand);
         // prefix at the start of this pair's run: X is non-decreasing, so the
         // latest run start carries the largest X
         const long long xr = block_inclusive_max(cand && !prev_cand ? x : -1, sh);
-        const int key = cand ? (int)((x - xr) / kMergeT) : -1;
+        const int key = cand ? (int)((x - xr) / mt) : -1;
         mg[threadIdx.x] = key;
         __syncthreads();
         const bool leader = cand && (threadIdx.x == 0 || mg[threadIdx.x - 1] != key);
@@ -2101,7 +2108,13 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
                 for (long long i = 0; i < el; ++i) const_cast<double *>(A.tmp)[ae + i] = pv;
             if (last) {
                 const long long len = ag + gl + el - agl;
-                small_push(A.Q, make_bseg(agl, len, dst_id, glo, bhi), st);
+                if (A.to_leaf && len > kUnitMax) {   // (the group's last thread queues it below)
+                    s_gap = 1;
+                    s_ag = agl;
+                    s_gl = len;
+                    s_blo = glo;
+                } else
+                    small_push(A.Q, make_bseg(agl, len, dst_id, glo, bhi), st);
             }
         }
         __syncthreads();   // mg reuse
@@ -2113,7 +2126,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
             t_gap = 1;
         }
         else if (gl <= kUnitMax) u_gap = 1;
-        else if (gl <= sort_cap(1)) small_push(A.Q, make_bseg(ag, gl, dst_id, blo, bhi), st);
+        else if (gl <= sort_cap(1) && !A.to_leaf) small_push(A.Q, make_bseg(ag, gl, dst_id, blo, bhi), st);
         else if (gl <= kSortMax) s_gap = 1;
         else if (gl <= kLocalMax) l_gap = 1;
         else g_gap = 1;
@@ -2158,7 +2171,7 @@ __device__ EmitOut emit_pairs(bool have, long long ag, long long gl, long long a
     }
     if (s_gap)
         q_publish(A.Q.sq, A.Q.sq_ready, A.Q.scap, (int)(sbase[3] + pk_get(xpk, kPkS, 11)),
-                  with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemSort), q_epoch(A.Q));
+                  with_kind(make_bseg(s_ag, s_gl, dst_id, s_blo, bhi), kItemSort), q_epoch(A.Q));
     if (l_gap) {
         const int i = (int)(sbase[1] + pk_get(xpk, kPkL, 11));
         Seg c = with_kind(make_bseg(ag, gl, dst_id, blo, bhi), kItemLocal);
@@ -3802,6 +3815,40 @@ static cudaStream_t body_stream()   // captures the device loop's body (per thre
 static std::atomic<int> g_dloop_broken{0};   // a failed device-loop capture: graphs without it from then on
 static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 
+// Staged scatter tiles per SM in one pass.  A tile costs ~3-4 us of fixed work
+// (class table, scan, one bulk copy per gap run), so one small array gets one
+// tile per SM (1M keys: 489 tiles of 2K keys -> 140 of 7K); large arrays and
+// batches keep KS_STAGE_ITEMS_PER_SM (tile capacity kStageMax keys).
+#ifndef KS_TO_LEAF
+#define KS_TO_LEAF 0   // measured: 1M +10%, 2M -3% (stragglers: groups up to 2x n / SMs keys); off
+#endif
+#ifndef KS_TO_LEAF_DIV
+#define KS_TO_LEAF_DIV 1
+#endif
+#ifndef KS_TO_LEAF_CAND4
+#define KS_TO_LEAF_CAND4 4
+#endif
+#ifndef KS_TO_LEAF_MAX_N
+#define KS_TO_LEAF_MAX_N 2400000
+#endif
+#ifndef KS_IPSM1_MAX_N
+#define KS_IPSM1_MAX_N 2400000
+#endif
+#ifndef KS_IPSM2_MAX_N
+#define KS_IPSM2_MAX_N 4800000
+#endif
+#ifndef KS_IPSM3_MAX_N
+#define KS_IPSM3_MAX_N 0
+#endif
+static int stage_items_per_sm(long long n, bool batch)
+{
+    if (batch) return KS_STAGE_ITEMS_PER_SM;
+    if (n <= KS_IPSM1_MAX_N) return 1;
+    if (n <= KS_IPSM2_MAX_N) return std::min(2, KS_STAGE_ITEMS_PER_SM);
+    if (n <= KS_IPSM3_MAX_N) return std::min(3, KS_STAGE_ITEMS_PER_SM);
+    return KS_STAGE_ITEMS_PER_SM;
+}
+
 int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0, void *ws, size_t ws_bytes,
               cudaStream_t user_stream, bool profile, FastResult *res, double *h_out)
 {
@@ -3839,7 +3886,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     const int g_scatter = (KS_PLAN_FORK && !profile) ? std::max(cfg->sms, cfg->g_scatter - KS_FORK_ROOM) : cfg->g_scatter;
     const int g_scan = sms * 2;
     // chunks per pass: the staged scatter gives every SM KS_STAGE_ITEMS_PER_SM tiles
-    const int pass_items = KS_STAGED ? sms * KS_STAGE_ITEMS_PER_SM : std::min(g_count, g_scatter);
+    const int pass_items = KS_STAGED ? sms * stage_items_per_sm(n, d_off != nullptr) : std::min(g_count, g_scatter);
     const int g_pivots = sms;
     Launcher K(stream, profile);
 
@@ -3939,6 +3986,13 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // queue ready words cleared before a level (its plan publishes sort items)
     auto clear_ready = [&]() { cudaMemsetAsync(Q.sq_ready, 0, sizeof(unsigned long long) * L.sq_cap, stream); };
     const int scatter_pf = n >= KS_PF_MIN_N ? 1 : 0;
+    // One small array (latency bound: ~1K-key gaps, fewer list items than sorter
+    // CTAs): the plan merges consecutive gaps into groups of about n / SMs keys
+    // and queues them for the leaf kernel, whose 1024-thread sorter finishes one
+    // group per SM in a single wave (1M keys: 30 -> ~12 us for the sorts).
+    const int to_leaf = (KS_TO_LEAF && d_off == nullptr && n <= KS_TO_LEAF_MAX_N) ? 1 : 0;
+    const int leaf_merge_t = to_leaf ? (int)std::min<long long>(std::max<long long>(n / (sms * KS_TO_LEAF_DIV), 1024), kSortMax / 2 - 256) : 0;
+    const int leaf_merge_cand = to_leaf ? std::max(leaf_merge_t * KS_TO_LEAF_CAND4 / 4, 1024) : 0;
     auto global_pass = [&]() {
         const double *src = (level & 1) ? tmp : keys;
         double *dst = (level & 1) ? keys : tmp;
@@ -3956,7 +4010,8 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         const int plan_mode = (profile || t_in_body) ? 0
                               : (KS_PLAN_FORK == 2 && (d_off != nullptr || n < KS_SINGLE_MIN_N)) ? 1 : KS_PLAN_FORK;
         const ForkRes *fr = plan_mode == 1 ? fork_res() : nullptr;
-        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, plan_mode ? 1 : 0};
+        EmitArgs A{segs[gcur ^ 1], nseg_next, L.seg_cap, Q, units, L.unit_cap, keys, tmp, 0, plan_mode ? 1 : 0,
+                   leaf_merge_cand, leaf_merge_t, to_leaf};
         if (!first_single)   // (done by k_front_lut)
             K.run(kPhPivots, [&] {
                 launch(k_seg_offsets, dim3(1), dim3(1024), 0, stream, segs[gcur], nseg_cur, st, L.mat_cap, L.ch_cap,
@@ -4039,7 +4094,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     // clear: the queue's ready words are cleared first (a launch whose epoch
     // may repeat: the device loop's body, the host loop after a replay)
     auto leaf = [&](HostStatus *sig) {
-        EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1, 0};
+        EmitArgs A{segs[gcur], &st->nseg[gcur], L.seg_cap, Q, units, L.unit_cap, keys, tmp, 1, 0, 0, 0, 0};
         K.run(kPhLeaf, [&] { launch_pdl(kPdlHeavy, k_leaf, dim3(g_leaf), dim3(kLeafThreads), kLeafSmem, stream, A, st, keys, tmp); });
         // the list sorters: chained behind the leaf kernel (programmatic launch),
         // their CTAs take the SMs the leaf's CTAs leave once no local partition is

@@ -81,7 +81,10 @@ constexpr int kKeysPerPivotLocal = KS_LOCAL_KPP;   // local partitions (children
 // passes over several segments keep chunks <= kChunk (a segment's last chunk
 // is short, so long chunks would unbalance them)
 constexpr int kChunk = 16384;
-constexpr int kChunkMin = 2048;
+#ifndef KS_CHUNK_MIN
+#define KS_CHUNK_MIN 2048
+#endif
+constexpr int kChunkMin = KS_CHUNK_MIN;
 constexpr int kChunkAlign = 512;
 constexpr int kChunkItemsMax = 2048;  // bound on the pass grid used for the chunk size
 constexpr int kCountThreads = 512;
