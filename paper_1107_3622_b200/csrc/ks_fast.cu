@@ -3158,8 +3158,18 @@ __global__ void __launch_bounds__(sort_threads(C), C == 0 ? KS_MINB0 : (C == 3 ?
         static_assert(kW * sidx_size(kUnitMax) <= SortSmem<C>::kA + SortSmem<C>::kCap, "unit scratch fits a + b");
         __syncthreads();
         double *sm = (SortSmem<C>::kA > 1 ? S.a : S.b) + (threadIdx.x >> 5) * sidx_size(kUnitMax);   // (a, b contiguous)
+        // claimed warp by warp: the CTAs that run out of segments first take them all,
+        // the last CTAs find none left (a fixed share per CTA put ~8 us of unit
+        // sorts behind the last segment)
         const int nu = st->nunits;
-        for (int d = blockIdx.x * kW + (threadIdx.x >> 5); d < nu; d += gridDim.x * kW) finish_item(units[d], keys, tmp, sm);
+        for (;;) {
+            int d = 0;
+            if ((threadIdx.x & 31) == 0) d = atomicAdd(&st->unit_next, 1);
+            d = __shfl_sync(0xffffffffu, d, 0);
+            if (d >= nu) break;
+            finish_item(units[d], keys, tmp, sm);
+            __syncwarp();
+        }
     }
     if (chained) asm volatile("griddepcontrol.wait;" ::: "memory");
 }
@@ -3478,7 +3488,7 @@ __global__ void k_leaf_reset(LeafQ Q, DevStatus *st, HostStatus *out, cudaGraphC
         st->pending = nhb;
         st->nhb = 0;
         st->lq_head = st->lqb_claim = st->sq_claim = st->sq_head = 0;
-        st->nsmall[0] = st->nsmall[1] = st->small_next[0] = st->small_next[1] = st->nunits = 0;
+        st->nsmall[0] = st->nsmall[1] = st->small_next[0] = st->small_next[1] = st->nunits = st->unit_next = 0;
         ++st->nleaves;
     }
     // Device-resident recursion (the reference's worklist, sort_core.py:184-198):

@@ -159,6 +159,8 @@ struct DevStatus {
     unsigned int neg_zero;            // saw -0.0
     int nseg[2];                      // segment counts of the two level tables
     int nunits;                       // warp work items (unit sorts, fills) of the current pass
+    int unit_next;                    // ... their work counter (warps of the last sorter kernel claim them)
+    int pad_units_;
     // on-chip work queues of the leaf kernel (local partitions, segment sorts)
     int lq_claim, lq_head;            // local queue: slots claimed by producers / taken by consumers
     int lqb_claim;                    // ... big local items (> kLocalBig), stored from the front (LPT)
