@@ -13,7 +13,9 @@ G, P = "gpurun_out", "profiles"
 for src, dst in [(f"bench_{tag}.json", f"{tag}_bench.json"), (f"bench_ref_{tag}.json", f"{tag}_bench_reference.json"),
                  (f"launches_{tag}.csv", f"{tag}_ncu_launches.csv"), (f"full_summary_{tag}.txt", f"{tag}_ncu_full_summary.txt"),
                  (f"configs_{tag}.json", f"{tag}_configs_time.json"), ("pytest_gpu.log", f"{tag}_pytest_gpu.log"),
-                 (f"scale_n_{tag}.jsonl", f"{tag}_scale_n.jsonl"), (f"launches_warm_{tag}.txt", f"{tag}_ncu_launches_warm_l2.txt")]:
+                 (f"scale_n_{tag}.jsonl", f"{tag}_scale_n.jsonl"), (f"counters_{tag}.csv", f"{tag}_ncu_counters.csv"),
+                 (f"counters_{tag}.txt", f"{tag}_ncu_counters.txt"), (f"adversarial_{tag}.json", f"{tag}_adversarial.json"),
+                 (f"exact_time_{tag}.json", f"{tag}_exact_paths_time.json"), (f"timeline_{tag}.txt", f"{tag}_timeline_c0.txt"), (f"launches_warm_{tag}.txt", f"{tag}_ncu_launches_warm_l2.txt")]:
     if os.path.exists(os.path.join(G, src)):
         shutil.copy(os.path.join(G, src), os.path.join(P, dst))
 # launch list of the last timed bench step
