@@ -60,6 +60,14 @@ def parse():
     return p.parse_args()
 
 
+def bench_config(n, kind, world):
+    """The workload both arms (this engine, --impl reference) are measured on."""
+    return {"workload": f"C0: 1 x {n:,} float64 {kind} keys per GPU", "n": n, "kind": kind,
+            "parallelism": f"replicas x{world}", "l2": "flushed (256 MiB write) before every step",
+            "timing": "CUDA events around one k_sort call per step; restore+flush outside",
+            "vs_baseline_ref": "paper Table 1 K-sort 10M = 8.2293 s (PAPER.md:95)"}
+
+
 def ncu_traffic(phase, n, kind):
     """DRAM bytes per launch of `phase` from the committed ncu --set full capture
     (profiles/ncu_traffic.json), when it was taken on this workload; else None."""
@@ -212,12 +220,14 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": value / PAPER_KSORT_10M_KEYS_PER_S,
         "dtype": "f64", "data": "synthetic (reference generator workload.generate, seed 20260816)",
-        "config": {"workload": f"C0: 1 x {n:,} float64 {args.kind} keys", "n": n, "kind": args.kind,
-                   "parallelism": f"{threads} host threads, one independent array each"},
+        "config": bench_config(n, args.kind, world),   # (the GPU arm's config, key for key)
+        "reference_arm": {"host_threads": threads, "arrays_per_step": threads,
+                          "timing": "host perf_counter around one step: every thread sorts its own full array"},
         "cpu_baseline": {"value": value, "unit": "keys/s", "cores": threads, "kind": "port",
                          "sample": f"{threads} threads x full {n:,}-key array per step, {args.steps} steps "
-                                   "(C restatement of sort_core.k_sort; the Python reference cannot run "
-                                   "on the GPU box)"},
+                                   "(C restatement of sort_core.k_sort: the reference is pure Python, no C "
+                                   "sources to build; its own CPython timings are in the GPU arm's "
+                                   "cpu_baseline.python_reference)"},
         "e2e": {"value": value, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -477,10 +487,7 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": value / PAPER_KSORT_10M_KEYS_PER_S, "dtype": "f64",
         "data": "synthetic (reference generator workload.generate, seed 20260816, device twin)",
-        "config": {"workload": f"C0: 1 x {n:,} float64 {args.kind} keys per GPU", "n": n, "kind": args.kind,
-                   "parallelism": f"replicas x{world}", "l2": "flushed (256 MiB write) before every step",
-                   "timing": "CUDA events around one k_sort call per step; restore+flush outside",
-                   "vs_baseline_ref": "paper Table 1 K-sort 10M = 8.2293 s (PAPER.md:95)"},
+        "config": bench_config(n, args.kind, world),
         "gpu_launches": launches,
         "correct": ok,
         # the north star's roofline: all bytes the engine's passes read and write

@@ -64,6 +64,12 @@ d = {"source": f"ncu --set full --clock-control none, C0 10M uniform01 (scripts/
                     sum((by[k]["dram_read_MB"] + by[k]["dram_write_MB"]) * 1e6 for k in v if k in by) /
                     max(1, len([k for k in v if k in by]))}
                 for p, v in phases.items()}}
+# whole sort: the heavy kernels of one sort (count, scatter, leaf, list sorters; the small
+# front / scan / plan / reset launches move < 3% of the bytes and are not in the capture)
+heavy = [k for k in kern if any(x in k["kernel"] for x in ("k_count", "k_scatter", "k_leaf", "k_segsort")) and
+         "reset" not in k["kernel"]]
+d["phases"]["sort"] = {"launches": len(heavy), "kernels": [k["kernel"] for k in heavy],
+                       "dram_bytes_per_launch": sum((k["dram_read_MB"] + k["dram_write_MB"]) * 1e6 for k in heavy)}
 json.dump(d, open(os.path.join(P, "ncu_traffic.json"), "w"), indent=1)
 print(open(os.path.join(P, f"{tag}_ncu_launches.txt")).read())
 print(json.dumps(d["phases"]))
