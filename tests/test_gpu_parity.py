@@ -530,6 +530,21 @@ def test_sizes_around_engine_limits():
         assert same_bits(host(t), np.sort(a)), n
 
 
+@pytest.mark.parametrize("n", [2_399_999, 2_400_001, 4_799_999, 4_800_001, 5_000_337])
+def test_sizes_around_tile_count_thresholds(n):
+    """One array gets 1 / 2 / 4 staged-scatter tiles per SM by its size (stage_items_per_sm in
+    ks_fast.cu): sizes on both sides of each switch, uniform keys and a skewed distribution
+    (chunks at the tile capacity, multi-level passes), sorted twice (direct launch, then the graph)."""
+    rng = np.random.default_rng(n)
+    for a in (rng.random(n), rng.exponential(1.0, n), np.floor(rng.random(n) * 300.0)):
+        want = np.sort(a)
+        t = dev(a)
+        for _ in range(2):
+            t.copy_(torch.from_numpy(a))
+            K.k_sort(t)
+            assert same_bits(host(t), want), n
+
+
 def test_sort_on_caller_side_stream():
     # the engine launches on the caller's current stream (sort_core._stream_ptr):
     # a sort issued under torch.cuda.stream(s) right after the input is produced
