@@ -91,6 +91,9 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #ifndef KS_SRC_CS
 #define KS_SRC_CS 1       // 1: the scatter's source loads are evict-first (ld.global.cs): C0 -3..5%
 #endif
+#ifndef KS_SRC_PF
+#define KS_SRC_PF 0        // 1: staged scatter prefetches the next tile's keys and classes into L2 during the copy-out
+#endif
 #ifndef KS_PF_MIN_N
 #define KS_PF_MIN_N 2500000   // scatter destinations are prefetched into L2 for calls of at least this many keys
 #endif                        // (measured: 1M/2M keys -9%/-6% without, 3M..10M +6..11% without)
@@ -1904,6 +1907,16 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
                 fetch_table(g, nx - g.ch_off, base_i);
                 prefetch_runs(g, base_i);
                 have = nx;
+#if KS_SRC_PF
+                // the next tile's keys and classes into L2 while this tile's runs leave:
+                // its staging loads (two dependent DRAM round trips per thread) then hit L2
+                if (tid == 0) {
+                    const long long nb = g.start + (long long)(nx - g.ch_off) * chunk;
+                    const long long nc = min((long long)chunk, g.len - (long long)(nx - g.ch_off) * chunk);
+                    l2_prefetch(src + nb, 8ull * (unsigned long long)nc);
+                    l2_prefetch(cls + nb, 2ull * (unsigned long long)nc);
+                }
+#endif
             }
         }
         // C. copy-out in tile order: lane l of a warp writes position w + l, so
