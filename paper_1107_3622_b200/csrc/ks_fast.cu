@@ -17,6 +17,7 @@
 // scatter -> plan; then local partition rounds (one CTA per segment) and one
 // warp-per-unit finishing launch.  No key crosses to the host; the host reads
 // one small status block per pass to decide whether another pass is needed.
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <atomic>
 #include <cfloat>
@@ -31,6 +32,7 @@
 #include "ks_sortnet.cuh"
 
 namespace ks {
+namespace cg = cooperative_groups;
 
 #ifdef KS_TRACE
 // optional phase-cycle instrumentation (build with KS_TRACE=1), read via ks_trace_read
@@ -3309,6 +3311,318 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
 }
 
 // ---------------------------------------------------------------------------
+// One small array in ONE cooperative launch (kInitLocalMax < n <= sms *
+// kSmallChunk): the eleven dependent launches of the general schedule (rank,
+// LUT, count, scan, scatter || plan, leaf, two list sorters, reset) cost
+// 3-10 us each whatever the size.  Here every SM takes one contiguous chunk
+// of the input and the same K-sort pass runs between grid barriers:
+//   0. the first P keys (K-sort's pivots) ranked, a few per CTA; status reset
+//      -- barrier --
+//   1. distinct pivots in shared memory; every key of the chunk classified by
+//      binary search (class 2r: gap below pivot r, 2r+1: equal to pivot r),
+//      gated (non-finite, signed zeros) and counted; the chunk's offset
+//      inside each gap taken from an atomicAdd on the gap's total (arrival
+//      order is as good as chunk order: equal keys are bitwise equal and every
+//      gap is sorted below)
+//      -- barrier --
+//   2. class starts by a scan of the 2k+1 class sizes (every CTA, in shared
+//      memory); gap keys scattered to tmp (equality runs are never moved)
+//      -- barrier --
+//   3. CTA b sorts the gaps that start in [b n/G, (b+1) n/G) on chip
+//      (segsort_one, consecutive gaps merged up to kSortMax keys with their
+//      pivots' runs) into the user buffer and fills the equality runs.
+// Rare leftovers -- a gap above kSortMax keys, a skewed bucket the on-chip
+// sorter hands back -- go to the next level's lists; k_leaf_reset behind this
+// kernel publishes the status and the host / device loop continues as usual.
+// ---------------------------------------------------------------------------
+constexpr int kSmallChunk = 10240;   // keys per CTA (their classes are kept in shared memory)
+constexpr int kSmallTab = 128;       // gaps per batch of the sort phase
+struct SmallWords {                  // scratch in the offsets array
+    double sorted[kPMax + 1];        // the ranked first P keys
+    double piv[kPMax + 2];           // distinct pivots
+    unsigned gtot[kPMax + 1];        // keys per gap
+    unsigned etot[kPMax + 1];        // keys per equality run
+    unsigned cs[2 * kPMax + 4];      // class starts; cs[2k+1] = n
+    int k;
+};
+struct SmallSmem {                   // phases 0-2 (overlaid by SortSmem<2> in phase 3)
+    double piv[kPMax + 2];
+    unsigned cs[2 * kPMax + 4];      // class histogram of the chunk, then the class starts
+    unsigned off[kPMax + 1];         // next destination per gap
+    unsigned short cls[kSmallChunk];
+    long long sh[33];
+    unsigned shu[33];
+};
+struct SmallTab {                    // behind SortSmem<2>: the gaps of the current batch
+    unsigned gs[kSmallTab], ge[kSmallTab], nx[kSmallTab];   // gap start, gap end (= run start), run end
+    double pv[kSmallTab], plo[kSmallTab];                   // the gap's pivot (upper bound), lower bound
+    int j0, j1;
+};
+constexpr size_t kSmallSmemBytes = cmax(sizeof(SortSmem<2>), sizeof(SmallSmem)) + sizeof(SmallTab) + 64;
+static_assert(kSmallSmemBytes <= 227 * 1024, "k_small's shared memory");
+static_assert(sizeof(SmallSmem) <= sizeof(SortSmem<2>), "the tab sits behind the sorter's buffers");
+
+__global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double *tmp, long long n, InitLists Lst,
+                                                          DevStatus *st, unsigned long long magic, SmallWords *W,
+                                                          Seg *gnext, int gnext_cap)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmallSmem &S = *reinterpret_cast<SmallSmem *>(smem_raw);
+    SortSmem<2> &SS = *reinterpret_cast<SortSmem<2> *>(smem_raw);
+    SmallTab &T = *reinterpret_cast<SmallTab *>(smem_raw + ((sizeof(SortSmem<2>) + 15) & ~size_t(15)));
+    const LeafQ &Q = Lst.Q;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int P = pivots_for(n, kPMax);
+    // ---- 0. rank the first P keys; reset the status and the totals ------------------
+    for (int i = tid; i < P; i += kLeafThreads) S.piv[i] = __ldcg(keys + i);
+    __syncthreads();
+    {
+        const int per = (P + G - 1) / G;
+        for (int q = wid; q < per; q += kLeafThreads / 32) {
+            const int i = b * per + q;
+            if (i >= P) break;
+            const double v = S.piv[i];
+            int r = 0;
+            for (int j = lane; j < P; j += 32) {
+                const double y = S.piv[j];
+                r += (y < v || (y == v && j < i)) ? 1 : 0;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+            if (lane == 0) W->sorted[r] = v;   // (NaN keys -- rejected by the gate -- may collide; all in range)
+        }
+    }
+    if (b == G - 1) {
+        seq_advance(Q, magic);
+        unsigned long long *w = reinterpret_cast<unsigned long long *>(st);
+        for (int i = tid; i < (int)(sizeof(DevStatus) / 8); i += kLeafThreads) w[i] = 0ull;
+        __syncthreads();
+        if (tid == 0) {
+            st->bad_index = kNoIndex;
+            st->no_item_pf = 1;
+            st->npasses = 1;
+        }
+    }
+    if (b == 0)
+        for (int i = tid; i <= P; i += kLeafThreads) W->gtot[i] = W->etot[i] = 0u;
+    __threadfence();
+    grid.sync();
+    // ---- 1. pivots, classify + gate + count, chunk offsets ---------------------------
+    long long carry = 0;
+    for (int base = 0; base < P; base += kLeafThreads) {
+        const int i = base + tid;
+        const double v = i < P ? __ldcg(W->sorted + i) : 0.0;
+        const int keep = (i < P && (i == 0 || v != __ldcg(W->sorted + i - 1))) ? 1 : 0;
+        long long tot;
+        const long long pos = block_exclusive_scan(keep, S.sh, &tot);
+        if (keep) S.piv[carry + pos] = v;
+        carry += tot;
+    }
+    const int k = (int)carry;
+    const int rows = 2 * k + 1;
+    for (int c = tid; c < rows + 1; c += kLeafThreads) S.cs[c] = 0u;
+    __syncthreads();
+    const long long chunk = (n + G - 1) / G;
+    const long long base = (long long)b * chunk;
+    const int cnt = (int)max(0ll, min(chunk, n - base));
+    {
+        long long bad = LLONG_MAX;
+        unsigned pz = 0, nz = 0;
+        constexpr int kU = 4;
+        for (int i0 = 0; i0 < cnt; i0 += kU * kLeafThreads) {
+            double v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * kLeafThreads + tid;
+                v[u] = i < cnt ? __ldcg(keys + base + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * kLeafThreads + tid;
+                if (i >= cnt) continue;
+                gate_one(v[u], base + i, bad, pz, nz);
+                int lo = 0, hi = k;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.piv[mid] < v[u]) lo = mid + 1; else hi = mid;
+                }
+                const int c = 2 * lo + ((lo < k && S.piv[lo] == v[u]) ? 1 : 0);
+                S.cls[i] = (unsigned short)c;
+                atomicAdd(&S.cs[c], 1u);
+            }
+        }
+        gate_flush(bad, pz, nz, st);
+    }
+    __syncthreads();
+    for (int g0 = 0; g0 <= k; g0 += 2 * kLeafThreads) {   // (two atomics in flight per thread)
+        const int ga = g0 + tid, gb = g0 + kLeafThreads + tid;
+        const unsigned ha = ga <= k ? S.cs[2 * ga] : 0u, hb = gb <= k ? S.cs[2 * gb] : 0u;
+        const unsigned pa = ha ? atomicAdd(&W->gtot[ga], ha) : 0u;
+        const unsigned pb = hb ? atomicAdd(&W->gtot[gb], hb) : 0u;
+        if (ga <= k) S.off[ga] = pa;
+        if (gb <= k) S.off[gb] = pb;
+    }
+    for (int j = tid; j < k; j += kLeafThreads) {
+        const unsigned h = S.cs[2 * j + 1];
+        if (h) atomicAdd(&W->etot[j], h);
+    }
+    __threadfence();
+    grid.sync();
+    // ---- 2. class starts, scatter ------------------------------------------------------
+    const bool ab = abort_requested(st);   // (every CTA's gate flags are in: uniform over the grid)
+    {
+        // sizes of classes 0..2k -> starts (4 per thread, one block scan); cs[2k+1] = n
+        unsigned sz[4];
+        unsigned t = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = 4 * tid + e;
+            sz[e] = c < rows ? ((c & 1) ? __ldcg(&W->etot[c >> 1]) : __ldcg(&W->gtot[c >> 1])) : 0u;
+            t += sz[e];
+        }
+        unsigned ex = block_exclusive_scan_u32(t, S.shu, nullptr);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int c = 4 * tid + e;
+            if (c <= rows) S.cs[c] = ex;
+            ex += sz[e];
+        }
+    }
+    __syncthreads();
+    for (int g = tid; g <= k; g += kLeafThreads) S.off[g] += S.cs[2 * g];
+    if (b == 0) {   // for the later batches of the sort phase
+        for (int c = tid; c <= rows; c += kLeafThreads) W->cs[c] = S.cs[c];
+        for (int j = tid; j < k; j += kLeafThreads) W->piv[j] = S.piv[j];
+        if (tid == 0) W->k = k;
+    }
+    __syncthreads();
+    if (!ab) {
+        constexpr int kU = 4;
+        for (int i0 = 0; i0 < cnt; i0 += kU * kLeafThreads) {
+            double v[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * kLeafThreads + tid;
+                v[u] = i < cnt ? __ldcg(keys + base + i) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int i = i0 + u * kLeafThreads + tid;
+                if (i >= cnt) continue;
+                const unsigned c = S.cls[i];
+                if (!(c & 1u)) tmp[atomicAdd(&S.off[c >> 1], 1u)] = v[u];
+            }
+        }
+    }
+    // my gaps: those that start in [b n / G, (b + 1) n / G); the first batch's table from shared memory
+    {
+        const unsigned lo_b = (unsigned)(((long long)b * n) / G), hi_b = (unsigned)(((long long)(b + 1) * n) / G);
+        if (tid == 0) {
+            int lo = 0, hi = k + 1;   // first gap j with cs[2j] >= lo_b
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (S.cs[2 * mid] < lo_b) lo = mid + 1; else hi = mid;
+            }
+            int j0 = lo;
+            hi = k + 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (S.cs[2 * mid] < hi_b) lo = mid + 1; else hi = mid;
+            }
+            // (a gap of zero keys at the very end starts at n: the last CTA takes it, it has no work)
+            T.j0 = j0;
+            T.j1 = b == G - 1 ? k + 1 : lo;
+        }
+        __syncthreads();
+        const int j0 = T.j0, j1 = T.j1;
+        for (int t = tid; t < kSmallTab && j0 + t < j1; t += kLeafThreads) {
+            const int j = j0 + t;
+            T.gs[t] = S.cs[2 * j];
+            T.ge[t] = S.cs[2 * j + 1];
+            T.nx[t] = j < k ? S.cs[2 * j + 2] : S.cs[2 * j + 1];
+            T.pv[t] = j < k ? S.piv[j] : CUDART_INF;
+            T.plo[t] = j > 0 ? S.piv[j - 1] : -CUDART_INF;
+        }
+    }
+    __threadfence();
+    grid.sync();
+    if (ab) return;
+    // ---- 3. sort my gaps ---------------------------------------------------------------
+    const int j0 = T.j0, j1 = T.j1;
+    unsigned long long keys_sorted = 0, segs_sorted = 0, keys_filled = 0;
+    for (int jb = j0; jb < j1; jb += kSmallTab) {
+        const int nt = min(kSmallTab, j1 - jb);
+        if (jb > j0) {   // later batches: from the arrays CTA 0 left in global memory
+            __syncthreads();
+            const int kk = __ldcg(&W->k);
+            for (int t = tid; t < nt; t += kLeafThreads) {
+                const int j = jb + t;
+                T.gs[t] = __ldcg(&W->cs[2 * j]);
+                T.ge[t] = __ldcg(&W->cs[2 * j + 1]);
+                T.nx[t] = j < kk ? __ldcg(&W->cs[2 * j + 2]) : T.ge[t];
+                T.pv[t] = j < kk ? __ldcg(&W->piv[j]) : CUDART_INF;
+                T.plo[t] = j > 0 ? __ldcg(&W->piv[j - 1]) : -CUDART_INF;
+            }
+            __syncthreads();
+        }
+        int t = 0;
+        while (t < nt) {   // (uniform over the CTA)
+            const unsigned a = T.gs[t];
+            unsigned e = T.ge[t];
+            int u = t + 1;
+            const bool big = e - a > (unsigned)kSortMax;
+            if (!big)
+                while (u < nt && T.ge[u] - a <= (unsigned)kSortMax) e = T.ge[u++];
+            // equality runs: inside the group they are part of its data (tmp); the last one is final
+            for (int q = t; q < u; ++q) {
+                const unsigned r0 = T.ge[q], r1 = T.nx[q];
+                double *dstp = (q + 1 < u) ? tmp : keys;
+                const double pv = T.pv[q];
+                for (unsigned i = r0 + tid; i < r1; i += kLeafThreads) dstp[i] = pv;
+                keys_filled += r1 - r0;
+            }
+            const unsigned len = e - a;
+            if (big) {   // (rare) more keys than the on-chip sorter holds: the next level takes the gap
+                if (tid == 0) {
+                    Seg c = make_seg(a, len, 1);
+                    c.stall = 4ll * len > 3ll * n ? 1 : 0;   // (presorted, reversed, ...: sampled pivots next)
+                    if (len > (unsigned)kLocalMax) {
+                        const int gi = atomicAdd(&st->nseg[1], 1);
+                        if (gi < gnext_cap) gnext[gi] = c; else st->overflow = 4;
+                    } else
+                        hb_push(Q, c, st);
+                }
+            } else if (len > (unsigned)kUnitMax) {
+                __syncthreads();   // the fills above and the previous segment's buffers
+                segsort_one<2>(SS, make_bseg(a, len, 1, T.plo[t], T.pv[u - 1]), Q, st, keys, tmp);
+                keys_sorted += len;
+                segs_sorted += 1;
+                __syncthreads();
+            } else if (len > 0) {
+                __syncthreads();
+                if (wid == 0) finish_item(make_item(a, len, kItemUnit, 1), keys, tmp, SS.b);
+                keys_sorted += len;
+                segs_sorted += 1;
+                __syncthreads();
+            }
+            t = u;
+        }
+    }
+    if (tid == 0) {
+        add_bytes(st, kPhLeaf, 16ull * keys_sorted + 8ull * keys_filled);
+        atomicAdd(&st->keys_leaf, keys_sorted);
+        atomicAdd(&st->leaves, segs_sorted);
+        if (b == 0) {
+            add_bytes(st, kPhCount, 8ull * (unsigned long long)n);
+            add_bytes(st, kPhScatter, 16ull * (unsigned long long)n);
+            atomicAdd(&st->keys_partitioned, (unsigned long long)n);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // host plumbing
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
@@ -3600,6 +3914,7 @@ static const EngineCfg *engine_cfg()
         smem(k_scatter2, sizeof(Scatter2Smem));
     }
     smem(k_leaf, kLeafSmem);
+    smem(k_small, kSmallSmemBytes);
     smem(k_segsort<0>, sort_smem<0>());
     smem(k_segsort<1>, sort_smem<1>());
     smem(k_segsort<3>, sort_smem<3>());
@@ -3854,6 +4169,12 @@ static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 #ifndef KS_TO_LEAF_MAX_N
 #define KS_TO_LEAF_MAX_N 2400000
 #endif
+#ifndef KS_COOP
+#define KS_COOP 1
+#endif
+#ifndef KS_COOP_MAX_N
+#define KS_COOP_MAX_N 1500000
+#endif
 #ifndef KS_IPSM1_MAX_N
 #define KS_IPSM1_MAX_N 2400000
 #endif
@@ -3958,6 +4279,10 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
     auto aborted = [&]() { return h.bad_index != kNoIndex || (h.pos_zero && h.neg_zero) || h.bad_arg; };
 
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
+    // one small array: rank, count, scatter and the on-chip sorts in one cooperative launch
+    const bool coop = KS_COOP && !profile && !KS_CHECK && d_off == nullptr && n > kInitLocalMax && n <= KS_COOP_MAX_N &&
+                      n <= (long long)sms * kSmallChunk && sizeof(SmallWords) <= sizeof(long long) * (size_t)L.mat_cap &&
+                      L.seg_cap >= 1;
     // level 0 of one array: its first P keys ranked into `sorted` (scratch in the
     // offsets array, written only later by the scan)
     bool rank_done = false;
@@ -4185,6 +4510,31 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
         if (KS_CHECK) {
             cudaMemsetAsync(cw, 0, sizeof(CheckWords), stream);
             k_check_sum<<<sms * 4, 256, 0, stream>>>(keys, n, &cw->in_sum, &cw->in_xor);
+        }
+        if (coop) {
+            // one small array: the whole first level in one cooperative launch (see k_small)
+            K.run(kPhLeaf, [&] {
+                cudaLaunchConfig_t lc = {};
+                lc.gridDim = dim3(sms);
+                lc.blockDim = dim3(kLeafThreads);
+                lc.dynamicSmemBytes = kSmallSmemBytes;
+                lc.stream = stream;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                cudaLaunchKernelEx(&lc, k_small, keys, tmp, n, Lst, st, ws_magic, reinterpret_cast<SmallWords *>(moff),
+                                   segs[1], L.seg_cap);
+            });
+            level = 1;
+            gcur = 1;
+            K.run(kPhGate, [&] {
+                launch(k_leaf_reset, dim3(1), dim3(256), 0, stream, Q, st, sig_spec, cond_h, cond_on ? 1 : 0, gcur);
+            });
+            ++Q.epoch;
+            ++leaves_run;
+            return;
         }
         init_launch();
         if (n > kInitLocalMax) global_pass();   // (its kernels exit at once when no segment is that long)
