@@ -3335,7 +3335,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
 // sorter hands back -- go to the next level's lists; k_leaf_reset behind this
 // kernel publishes the status and the host / device loop continues as usual.
 // ---------------------------------------------------------------------------
-constexpr int kSmallChunk = 10240;   // keys per CTA (their classes are kept in shared memory)
+#ifndef KS_SMALL_CHUNK
+#define KS_SMALL_CHUNK 16896
+#endif
+constexpr int kSmallChunk = KS_SMALL_CHUNK;   // keys per CTA (their classes are kept in shared memory)
 constexpr int kSmallTab = 128;       // gaps per batch of the sort phase
 struct SmallWords {                  // scratch in the offsets array
     double sorted[kPMax + 1];        // the ranked first P keys
@@ -3357,6 +3360,10 @@ struct SmallTab {                    // behind SortSmem<2>: the gaps of the curr
     unsigned gs[kSmallTab], ge[kSmallTab], nx[kSmallTab];   // gap start, gap end (= run start), run end
     double pv[kSmallTab], plo[kSmallTab];                   // the gap's pivot (upper bound), lower bound
     int j0, j1;
+    unsigned lo, hi;           // my destination range [b n / G, (b + 1) n / G)
+    unsigned pre_start, pre_end;   // the part inside my range of the equality run of the last gap that starts before it
+    double pre_pv;
+    unsigned maxgap;
 };
 constexpr size_t kSmallSmemBytes = cmax(sizeof(SortSmem<2>), sizeof(SmallSmem)) + sizeof(SmallTab) + 64;
 static_assert(kSmallSmemBytes <= 227 * 1024, "k_small's shared memory");
@@ -3490,14 +3497,23 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
             ex += sz[e];
         }
     }
+    if (tid == 0) T.maxgap = 0u;
     __syncthreads();
-    for (int g = tid; g <= k; g += kLeafThreads) S.off[g] += S.cs[2 * g];
+    for (int g = tid; g <= k; g += kLeafThreads) {
+        S.off[g] += S.cs[2 * g];
+        atomicMax(&T.maxgap, S.cs[2 * g + 1] - S.cs[2 * g]);
+    }
     if (b == 0) {   // for the later batches of the sort phase
         for (int c = tid; c <= rows; c += kLeafThreads) W->cs[c] = S.cs[c];
         for (int j = tid; j < k; j += kLeafThreads) W->piv[j] = S.piv[j];
         if (tid == 0) W->k = k;
     }
     __syncthreads();
+    // One gap kept > 3/4 of the keys (presorted, reversed, organ-pipe inputs: the first P keys
+    // are no sample of the array): this level is void -- the keys go to tmp as they are and the
+    // whole array becomes one stalled segment of the next level, whose pivots are sampled
+    // across it (the stall guard of the general pass).
+    const bool degenerate = 4ull * T.maxgap > 3ull * (unsigned long long)n;
     if (!ab) {
         constexpr int kU = 4;
         for (int i0 = 0; i0 < cnt; i0 += kU * kLeafThreads) {
@@ -3512,8 +3528,17 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
                 const int i = i0 + u * kLeafThreads + tid;
                 if (i >= cnt) continue;
                 const unsigned c = S.cls[i];
-                if (!(c & 1u)) tmp[atomicAdd(&S.off[c >> 1], 1u)] = v[u];
+                if (degenerate) tmp[base + i] = v[u];
+                else if (!(c & 1u)) tmp[atomicAdd(&S.off[c >> 1], 1u)] = v[u];
             }
+        }
+        if (degenerate && b == 0 && tid == 0) {
+            Seg c = make_seg(0, n, 1);
+            c.stall = 1;
+            if (gnext_cap >= 1) gnext[0] = c; else st->overflow = 4;
+            st->nseg[1] = 1;
+            add_bytes(st, kPhCount, 8ull * (unsigned long long)n);
+            add_bytes(st, kPhScatter, 16ull * (unsigned long long)n);
         }
     }
     // my gaps: those that start in [b n / G, (b + 1) n / G); the first batch's table from shared memory
@@ -3532,8 +3557,22 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
                 if (S.cs[2 * mid] < hi_b) lo = mid + 1; else hi = mid;
             }
             // (a gap of zero keys at the very end starts at n: the last CTA takes it, it has no work)
-            T.j0 = j0;
-            T.j1 = b == G - 1 ? k + 1 : lo;
+            T.j0 = degenerate ? 0 : j0;
+            T.j1 = degenerate ? 0 : (b == G - 1 ? k + 1 : lo);
+            T.lo = lo_b;
+            T.hi = b == G - 1 ? (unsigned)n : hi_b;
+            // the equality run between the last gap that starts before my range and gap j0 (the first
+            // that starts inside it): its owner fills what lies in its own range, I fill my part
+            T.pre_start = T.pre_end = lo_b;
+            T.pre_pv = 0.0;
+            if (!degenerate && j0 >= 1 && j0 - 1 < k) {
+                const unsigned r0 = max(S.cs[2 * (j0 - 1) + 1], lo_b), r1 = min(S.cs[2 * (j0 - 1) + 2], T.hi);
+                if (r1 > r0) {
+                    T.pre_start = r0;
+                    T.pre_end = r1;
+                    T.pre_pv = S.piv[j0 - 1];
+                }
+            }
         }
         __syncthreads();
         const int j0 = T.j0, j1 = T.j1;
@@ -3551,7 +3590,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
     if (ab) return;
     // ---- 3. sort my gaps ---------------------------------------------------------------
     const int j0 = T.j0, j1 = T.j1;
+    const unsigned my_hi = T.hi;
     unsigned long long keys_sorted = 0, segs_sorted = 0, keys_filled = 0;
+    // long equality runs are filled range by range: each CTA writes the part inside its own range
+    for (unsigned i = T.pre_start + tid; i < T.pre_end; i += kLeafThreads) keys[i] = T.pre_pv;
+    keys_filled += T.pre_end - T.pre_start;
     for (int jb = j0; jb < j1; jb += kSmallTab) {
         const int nt = min(kSmallTab, j1 - jb);
         if (jb > j0) {   // later batches: from the arrays CTA 0 left in global memory
@@ -3576,9 +3619,11 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
             if (!big)
                 while (u < nt && T.ge[u] - a <= (unsigned)kSortMax) e = T.ge[u++];
             // equality runs: inside the group they are part of its data (tmp); the last one is final
+            // (a final run that leaves my range is continued by the CTAs it reaches into)
             for (int q = t; q < u; ++q) {
-                const unsigned r0 = T.ge[q], r1 = T.nx[q];
-                double *dstp = (q + 1 < u) ? tmp : keys;
+                const bool inside = q + 1 < u;
+                const unsigned r0 = T.ge[q], r1 = inside ? T.nx[q] : min(T.nx[q], max(my_hi, r0));
+                double *dstp = inside ? tmp : keys;
                 const double pv = T.pv[q];
                 for (unsigned i = r0 + tid; i < r1; i += kLeafThreads) dstp[i] = pv;
                 keys_filled += r1 - r0;
@@ -3614,7 +3659,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
         add_bytes(st, kPhLeaf, 16ull * keys_sorted + 8ull * keys_filled);
         atomicAdd(&st->keys_leaf, keys_sorted);
         atomicAdd(&st->leaves, segs_sorted);
-        if (b == 0) {
+        if (b == 0 && !degenerate) {
             add_bytes(st, kPhCount, 8ull * (unsigned long long)n);
             add_bytes(st, kPhScatter, 16ull * (unsigned long long)n);
             atomicAdd(&st->keys_partitioned, (unsigned long long)n);
@@ -4172,8 +4217,11 @@ static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 #ifndef KS_COOP
 #define KS_COOP 1
 #endif
+#ifndef KS_COOP_MIN_N
+#define KS_COOP_MIN_N 2048
+#endif
 #ifndef KS_COOP_MAX_N
-#define KS_COOP_MAX_N 1500000
+#define KS_COOP_MAX_N 2000000
 #endif
 #ifndef KS_IPSM1_MAX_N
 #define KS_IPSM1_MAX_N 2400000
@@ -4280,7 +4328,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
     // one small array: rank, count, scatter and the on-chip sorts in one cooperative launch
-    const bool coop = KS_COOP && !profile && !KS_CHECK && d_off == nullptr && n > kInitLocalMax && n <= KS_COOP_MAX_N &&
+    const bool coop = KS_COOP && !profile && !KS_CHECK && d_off == nullptr && n > KS_COOP_MIN_N && n <= KS_COOP_MAX_N &&
                       n <= (long long)sms * kSmallChunk && sizeof(SmallWords) <= sizeof(long long) * (size_t)L.mat_cap &&
                       L.seg_cap >= 1;
     // level 0 of one array: its first P keys ranked into `sorted` (scratch in the

@@ -545,6 +545,78 @@ def test_sizes_around_tile_count_thresholds(n):
             assert same_bits(host(t), want), n
 
 
+def _small_case(kind, n, rng):
+    if kind == "uniform":
+        return rng.random(n)
+    if kind == "dup256":
+        return np.floor(rng.random(n) * 256.0) / 256.0
+    if kind == "three_values":      # equality runs far longer than one CTA's range, empty gaps
+        return rng.integers(0, 3, n).astype(np.float64)
+    if kind == "constant":
+        return np.full(n, 0.375)
+    if kind == "presorted":
+        return np.arange(n, dtype=np.float64)
+    if kind == "reversed":
+        return np.arange(n, 0, -1).astype(np.float64)
+    if kind == "organ":
+        h = n // 2
+        return np.concatenate([np.arange(h), np.arange(n - h, 0, -1)]).astype(np.float64)
+    if kind == "one_big_gap":       # 60% of the keys between two neighbouring pivots (not a stall: < 3/4)
+        a = rng.random(n)
+        m = rng.random(n) < 0.6
+        m[:4096] = False
+        a[m] = 0.5 + rng.random(int(m.sum())) * 1e-9
+        return a
+    if kind == "sorted_prefix":     # the first P keys are the smallest: ~P empty gaps in the first CTA's range
+        a = rng.random(n) + 1.0
+        m = min(4096, n // 2)
+        a[:m] = np.sort(rng.random(m))
+        return a
+    if kind == "lognormal":
+        return rng.lognormal(0.0, 4.0, n)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["uniform", "dup256", "three_values", "constant", "presorted", "reversed", "organ",
+                                  "one_big_gap", "sorted_prefix", "lognormal"])
+@pytest.mark.parametrize("n", [2049, 5000, 24_577, 150_001, 1_000_003, 1_999_999])
+def test_small_array_cooperative_path(kind, n):
+    """One array of 2K..2M keys sorts in one cooperative launch (k_small in ks_fast.cu): equality runs
+    that span several CTAs' ranges, gaps above the on-chip sorter's capacity (next level), the stall
+    bail-out (presorted / reversed / organ-pipe), batches of more than 128 gaps per CTA -- called three
+    times (direct launch, graph capture, replay), bytewise against numpy."""
+    rng = np.random.default_rng(zlib.crc32(f"small/{kind}/{n}".encode()))
+    a = _small_case(kind, n, rng)
+    want = np.sort(a)
+    t = dev(a)
+    for _ in range(3):
+        t.copy_(torch.from_numpy(a))
+        K.k_sort(t)
+        assert same_bits(host(t), want), (kind, n)
+
+
+@pytest.mark.parametrize("n", [2049, 30_000, 400_000, 1_700_000])
+def test_small_array_cooperative_path_rejections(n):
+    """Non-finite keys (first, middle, last CTA's chunk) leave the buffer untouched; mixed signed
+    zeros rerun in the exact engine (bytes equal to the reference K-sort's)."""
+    rng = np.random.default_rng(n)
+    for pos in (0, n // 2, n - 1):
+        a = rng.random(n)
+        a[pos] = np.nan if pos != n // 2 else np.inf
+        t = dev(a)
+        with pytest.raises(K.NonFiniteKeyError) as ei:
+            K.k_sort(t)
+        assert f"index {pos} " in str(ei.value)
+        assert same_bits(host(t), a)
+    if n <= 30_000:
+        a = rng.random(n)
+        a[::7] = 0.0
+        a[3::7] = -0.0
+        t = dev(a)
+        K.k_sort(t)
+        assert same_bits(host(t), oracle_ksort(a))
+
+
 def test_sort_on_caller_side_stream():
     # the engine launches on the caller's current stream (sort_core._stream_ptr):
     # a sort issued under torch.cuda.stream(s) right after the input is produced
