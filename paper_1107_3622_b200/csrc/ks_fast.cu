@@ -4328,7 +4328,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
     // one small array: rank, count, scatter and the on-chip sorts in one cooperative launch
-    const bool coop = KS_COOP && !profile && !KS_CHECK && d_off == nullptr && n > KS_COOP_MIN_N && n <= KS_COOP_MAX_N &&
+    const bool coop = KS_COOP && !profile && d_off == nullptr && n > KS_COOP_MIN_N && n <= KS_COOP_MAX_N &&
                       n <= (long long)sms * kSmallChunk && sizeof(SmallWords) <= sizeof(long long) * (size_t)L.mat_cap &&
                       L.seg_cap >= 1;
     // level 0 of one array: its first P keys ranked into `sorted` (scratch in the
