@@ -2508,7 +2508,7 @@ struct SortSmem {
     alignas(16) double b[kCap + 2];   // bucket order, from b[start & 1] (sorted in place; TMA source)
     unsigned cur[kBuckets];
     int big[kBigCap];
-    double red[2][32];
+    double red[3][32];     // block min / max / scaled sum
     double bounds[2];      // lo, scale
     int bits;              // bucket map in the order-preserving bit image (wide segments)
     unsigned sh[33];
@@ -2728,7 +2728,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         }
         __syncthreads();
     }
-    double mn = CUDART_INF, mx = -CUDART_INF;
+    double mn = CUDART_INF, mx = -CUDART_INF, sm16 = 0.0;   // (sm16: sum of key * 2^-16, for the mean)
     for (int i0 = 0; !fused && i0 < m; i0 += kLU * kT) {
         double x[kLU];
 #pragma unroll
@@ -2743,6 +2743,7 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
                 if (!Smem::kSingle) S.a[i] = x[u];
                 mn = x[u] < mn ? x[u] : mn;
                 mx = x[u] > mx ? x[u] : mx;
+                sm16 += x[u] * 0x1p-16;
             }
         }
     }
@@ -2751,11 +2752,13 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
         const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
         mn = p < mn ? p : mn;
         mx = q > mx ? q : mx;
+        sm16 += __shfl_xor_sync(0xffffffffu, sm16, o);
     }
     if (!fused) {
     if (lane == 0) {
         S.red[0][wid] = mn;
         S.red[1][wid] = mx;
+        S.red[2][wid] = sm16;
     }
 #pragma unroll 1
     for (int b = tid; b < B; b += kT) S.cur[b] = 0u;
@@ -2767,16 +2770,23 @@ __device__ void segsort_one(SortSmem<C> &S, const Seg &g, const LeafQ &Q, DevSta
     if (wid == 0) {   // block min / max and the bucket scale, broadcast through shared memory
         mn = lane < kWarps ? S.red[0][lane] : CUDART_INF;
         mx = lane < kWarps ? S.red[1][lane] : -CUDART_INF;
+        sm16 = lane < kWarps ? S.red[2][lane] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             const double p = __shfl_xor_sync(0xffffffffu, mn, o), q = __shfl_xor_sync(0xffffffffu, mx, o);
             mn = p < mn ? p : mn;
             mx = q > mx ? q : mx;
+            sm16 += __shfl_xor_sync(0xffffffffu, sm16, o);
         }
         if (lane == 0) {
             double scale = mx > mn ? (double)B / (mx - mn) : -1.0;            // -1: constant segment
             int bits = 0;
-            const bool wide = (mn > 0.0 && mx > 64.0 * mn) || (mx < 0.0 && mn < 64.0 * mx);
+            // many binades: log-like data (bit-image buckets) -- unless the keys do not crowd the
+            // small-magnitude end: a mean at least 1/8 of the range away from it (uniform keys down
+            // to ~0: the array's lowest gap) keeps the linear map
+            const double mean16 = sm16 / (double)m, lo16 = mn * 0x1p-16, hi16 = mx * 0x1p-16;
+            const bool spread = mn > 0.0 ? (mean16 - lo16 > (hi16 - lo16) * 0.125) : (hi16 - mean16 > (hi16 - lo16) * 0.125);
+            const bool wide = ((mn > 0.0 && mx > 64.0 * mn) || (mx < 0.0 && mn < 64.0 * mx)) && !spread;
             if (mx > mn && (wide || !(scale > 0.0) || isinf(scale))) {
                 bits = 1;   // many binades, or a range the linear map cannot hold
                 scale = (double)B / (double)(ord_bits(mx) - ord_bits(mn));
@@ -3335,11 +3345,15 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
 // sorter hands back -- go to the next level's lists; k_leaf_reset behind this
 // kernel publishes the status and the host / device loop continues as usual.
 // ---------------------------------------------------------------------------
+#ifndef KS_SMALL_KPP
+#define KS_SMALL_KPP 1024
+#endif
 #ifndef KS_SMALL_CHUNK
 #define KS_SMALL_CHUNK 16896
 #endif
 constexpr int kSmallChunk = KS_SMALL_CHUNK;   // keys per CTA (their classes are kept in shared memory)
 constexpr int kSmallTab = 128;       // gaps per batch of the sort phase
+constexpr int kSmallLut = 1024;      // value buckets of the classification's search-range table
 struct SmallWords {                  // scratch in the offsets array
     double sorted[kPMax + 1];        // the ranked first P keys
     double piv[kPMax + 2];           // distinct pivots
@@ -3353,6 +3367,7 @@ struct SmallSmem {                   // phases 0-2 (overlaid by SortSmem<2> in p
     unsigned cs[2 * kPMax + 4];      // class histogram of the chunk, then the class starts
     unsigned off[kPMax + 1];         // next destination per gap
     unsigned short cls[kSmallChunk];
+    unsigned short lut[kSmallLut + 2];   // lut[t]: pivots whose value bucket is below t (search range of a key in bucket t)
     long long sh[33];
     unsigned shu[33];
 };
@@ -3381,7 +3396,17 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
     const LeafQ &Q = Lst.Q;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int G = gridDim.x, b = blockIdx.x;
-    const int P = pivots_for(n, kPMax);
+    const int P = pivots_for(n, kPMax, KS_SMALL_KPP);   // (more pivots than the general pass: evener shares per CTA)
+#ifdef KS_TIMELINE
+    unsigned long long tl_p = tl_now();
+#define KS_TLP(id)                                   \
+    do {                                             \
+        if (threadIdx.x == 0) tl_rec(id, 8, 0, tl_p); \
+        tl_p = tl_now();                             \
+    } while (0)
+#else
+#define KS_TLP(id)
+#endif
     // ---- 0. rank the first P keys; reset the status and the totals ------------------
     for (int i = tid; i < P; i += kLeafThreads) S.piv[i] = __ldcg(keys + i);
     __syncthreads();
@@ -3415,7 +3440,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
     if (b == 0)
         for (int i = tid; i <= P; i += kLeafThreads) W->gtot[i] = W->etot[i] = 0u;
     __threadfence();
+    KS_TLP(40);
     grid.sync();
+    KS_TLP(44);
     // ---- 1. pivots, classify + gate + count, chunk offsets ---------------------------
     long long carry = 0;
     for (int base = 0; base < P; base += kLeafThreads) {
@@ -3430,6 +3457,20 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
     const int k = (int)carry;
     const int rows = 2 * k + 1;
     for (int c = tid; c < rows + 1; c += kLeafThreads) S.cs[c] = 0u;
+    // search-range table: value buckets t(v) = (v - piv[0]) * scale (monotone in v, saturating, NaN -> 0);
+    // pivots of lower buckets are below a key of bucket t, pivots of higher ones above it
+    const double lut_lo = k > 0 ? S.piv[0] : 0.0;
+    double lut_scale = k > 1 ? (double)kSmallLut / (S.piv[k - 1] - lut_lo) : 0.0;
+    if (!(lut_scale > 0.0) || !isfinite(lut_scale)) lut_scale = 0.0;   // (one bucket: plain binary search)
+    auto vbucket = [&](double v) { return min(max(__double2int_rz((v - lut_lo) * lut_scale), 0), kSmallLut - 1); };
+    for (int t = tid; t <= kSmallLut; t += kLeafThreads) {
+        int lo = 0, hi = k;   // first pivot whose bucket is >= t
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (vbucket(S.piv[mid]) < t) lo = mid + 1; else hi = mid;
+        }
+        S.lut[t] = (unsigned short)lo;
+    }
     __syncthreads();
     const long long chunk = (n + G - 1) / G;
     const long long base = (long long)b * chunk;
@@ -3450,7 +3491,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
                 const int i = i0 + u * kLeafThreads + tid;
                 if (i >= cnt) continue;
                 gate_one(v[u], base + i, bad, pz, nz);
-                int lo = 0, hi = k;
+                const int tb = vbucket(v[u]);
+                int lo = S.lut[tb], hi = S.lut[tb + 1];
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
                     if (S.piv[mid] < v[u]) lo = mid + 1; else hi = mid;
@@ -3476,7 +3518,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
         if (h) atomicAdd(&W->etot[j], h);
     }
     __threadfence();
+    KS_TLP(41);
     grid.sync();
+    KS_TLP(44);
     // ---- 2. class starts, scatter ------------------------------------------------------
     const bool ab = abort_requested(st);   // (every CTA's gate flags are in: uniform over the grid)
     {
@@ -3586,7 +3630,9 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
         }
     }
     __threadfence();
+    KS_TLP(42);
     grid.sync();
+    KS_TLP(44);
     if (ab) return;
     // ---- 3. sort my gaps ---------------------------------------------------------------
     const int j0 = T.j0, j1 = T.j1;
@@ -3655,6 +3701,8 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
             t = u;
         }
     }
+    KS_TLP(43);
+#undef KS_TLP
     if (tid == 0) {
         add_bytes(st, kPhLeaf, 16ull * keys_sorted + 8ull * keys_filled);
         atomicAdd(&st->keys_leaf, keys_sorted);

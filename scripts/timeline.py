@@ -61,7 +61,8 @@ for r in recs:
     r["t0"] -= T0
     r["t1"] -= T0
 names = {30: "mark0", 31: "mark1", 2: "k_leaf", 10: "segsort<0>", 11: "segsort<1>", 13: "segsort<3>", 14: "segsort<4>", 20: "init_pass", 22: "front_lut",
-         21: "pivot_rank", 23: "count2", 24: "scan", 25: "plan", 26: "scatter2", 27: "leaf_reset"}
+         21: "pivot_rank", 23: "count2", 24: "scan", 25: "plan", 26: "scatter2", 27: "leaf_reset", 40: "small:rank", 41: "small:count", 42: "small:scatter",
+         43: "small:sort", 44: "small:barrier"}
 print(f"n={n} kind={kind} records={m} event span {ev_ms*1e3:.1f} us")
 mk = {r["kernel"]: r for r in recs if r["kernel"] in (30, 31)}
 if 30 in mk and 31 in mk:
