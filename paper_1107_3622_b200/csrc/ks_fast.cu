@@ -3349,7 +3349,7 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_leaf(EmitArgs A, DevStatus 
 #define KS_SMALL_KPP 1024
 #endif
 #ifndef KS_SMALL_CHUNK
-#define KS_SMALL_CHUNK 16896
+#define KS_SMALL_CHUNK 33792
 #endif
 constexpr int kSmallChunk = KS_SMALL_CHUNK;   // keys per CTA (their classes are kept in shared memory)
 constexpr int kSmallTab = 128;       // gaps per batch of the sort phase
@@ -4269,7 +4269,7 @@ static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 #define KS_COOP_MIN_N 2048
 #endif
 #ifndef KS_COOP_MAX_N
-#define KS_COOP_MAX_N 2000000
+#define KS_COOP_MAX_N 5000000
 #endif
 #ifndef KS_IPSM1_MAX_N
 #define KS_IPSM1_MAX_N 2400000

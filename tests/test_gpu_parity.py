@@ -579,9 +579,9 @@ def _small_case(kind, n, rng):
 
 @pytest.mark.parametrize("kind", ["uniform", "dup256", "three_values", "constant", "presorted", "reversed", "organ",
                                   "one_big_gap", "sorted_prefix", "lognormal"])
-@pytest.mark.parametrize("n", [2049, 5000, 24_577, 150_001, 1_000_003, 1_999_999])
+@pytest.mark.parametrize("n", [2049, 5000, 24_577, 150_001, 1_000_003, 1_999_999, 4_999_999, 5_000_001])
 def test_small_array_cooperative_path(kind, n):
-    """One array of 2K..2M keys sorts in one cooperative launch (k_small in ks_fast.cu): equality runs
+    """One array of 2K..5M keys sorts in one cooperative launch (k_small in ks_fast.cu): equality runs
     that span several CTAs' ranges, gaps above the on-chip sorter's capacity (next level), the stall
     bail-out (presorted / reversed / organ-pipe), batches of more than 128 gaps per CTA -- called three
     times (direct launch, graph capture, replay), bytewise against numpy."""
