@@ -3408,6 +3408,10 @@ __global__ void __launch_bounds__(kLeafThreads, 1) k_small(double *keys, double 
 #define KS_TLP(id)
 #endif
     // ---- 0. rank the first P keys; reset the status and the totals ------------------
+    if (tid == 0) {   // my chunk into L2 while the pivots are ranked (its loads come two barriers later)
+        const long long ch0 = (n + G - 1) / G, b0 = (long long)b * ch0;
+        if (b0 < n) l2_prefetch(keys + b0, 8ull * (unsigned long long)min(ch0, n - b0));
+    }
     for (int i = tid; i < P; i += kLeafThreads) S.piv[i] = __ldcg(keys + i);
     __syncthreads();
     {
