@@ -3985,6 +3985,7 @@ FastLayout fast_layout(long long n, long long nseg0)
 struct EngineCfg {
     int sms, g_count, g_scatter, g_leaf, g_small[2], g_small3, g_small4;
     int g_count2, g_scatter2;
+    int coop_ok;   // k_small can run: cooperative launches supported and one CTA per SM fits
 };
 
 static const EngineCfg *engine_cfg()
@@ -4011,7 +4012,9 @@ static const EngineCfg *engine_cfg()
         smem(k_scatter2, sizeof(Scatter2Smem));
     }
     smem(k_leaf, kLeafSmem);
-    smem(k_small, kSmallSmemBytes);
+    const bool small_attr = cudaFuncSetAttribute(k_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)kSmallSmemBytes) == cudaSuccess;
+    if (!small_attr) cudaGetLastError();   // (the general schedule serves every size)
     smem(k_segsort<0>, sort_smem<0>());
     smem(k_segsort<1>, sort_smem<1>());
     smem(k_segsort<3>, sort_smem<3>());
@@ -4037,6 +4040,12 @@ static const EngineCfg *engine_cfg()
     c.g_small[1] = grid(k_segsort<1>, sort_threads(1), sort_smem<1>());
     c.g_small3 = grid(k_segsort<3>, sort_threads(3), sort_smem<3>());
     c.g_small4 = grid(k_segsort<4>, sort_threads(4), sort_smem<4>());
+    {
+        int coop = 0, occ = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        if (small_attr) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_small, kLeafThreads, kSmallSmemBytes);
+        c.coop_ok = (small_attr && coop && occ >= 1) ? 1 : 0;
+    }
     cfgs[dev] = c;
     ready[dev] = true;
     return &cfgs[dev];
@@ -4380,7 +4389,7 @@ int fast_sort(double *keys, long long n, const long long *d_off, long long nseg0
 
     const InitLists Lst{segs[0], Q, units, L.seg_cap, L.unit_cap};
     // one small array: rank, count, scatter and the on-chip sorts in one cooperative launch
-    const bool coop = KS_COOP && !profile && d_off == nullptr && n > KS_COOP_MIN_N && n <= KS_COOP_MAX_N &&
+    const bool coop = KS_COOP && cfg->coop_ok && !profile && d_off == nullptr && n > KS_COOP_MIN_N && n <= KS_COOP_MAX_N &&
                       n <= (long long)sms * kSmallChunk && sizeof(SmallWords) <= sizeof(long long) * (size_t)L.mat_cap &&
                       L.seg_cap >= 1;
     // level 0 of one array: its first P keys ranked into `sorted` (scratch in the

@@ -595,6 +595,23 @@ def test_small_array_cooperative_path(kind, n):
         assert same_bits(host(t), want), (kind, n)
 
 
+@pytest.mark.parametrize("n", [3000, 100_000, 1_000_000, 5_000_000])
+def test_small_array_takes_two_launches(n):
+    """Uniform arrays of 2K..5M keys finish in two kernels (k_small + the reset / status kernel) and one
+    host wait -- the general schedule takes eleven launches (ks_status_t.launches, host_syncs)."""
+    from paper_1107_3622_b200.sort_core import _sort_device
+    p = K.generate_device(n, 20260816)
+    want = torch.sort(p).values
+    for call in range(3):   # direct launch, graph capture, replay
+        t = p.clone()
+        st = _sort_device(t)
+        assert torch.equal(t, want)
+        assert int(st.launches) == 2 and int(st.host_syncs) == 1, (call, int(st.launches), int(st.host_syncs))
+    big = K.generate_device(5_000_001, 20260816)
+    st = _sort_device(big)
+    assert int(st.launches) > 2
+
+
 @pytest.mark.parametrize("n", [2049, 30_000, 400_000, 1_700_000])
 def test_small_array_cooperative_path_rejections(n):
     """Non-finite keys (first, middle, last CTA's chunk) leave the buffer untouched; mixed signed
