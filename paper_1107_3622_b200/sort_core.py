@@ -387,7 +387,6 @@ def ksort_partition(a: ArrayLike, left: int, right: int,
     return PartitionOutcome(pivot_index=int(piv.value), flag_used=bool(flag.value))
 
 
-@_on_input_device
 def k_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     """Sort a ascending, in place (sort_core.py:169-217), on the GPU.
 
@@ -396,9 +395,16 @@ def k_sort(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     """
     if (counts is None and type(a) is torch.Tensor and a.is_cuda and a.dtype is torch.float64 and a.dim() == 1
             and a.is_contiguous() and _raw_stream is not None):
-        # (the wrapper made a's device current; a failed fast call wrote nothing: the general path reruns it)
-        if _sort_device_fast(a, a.numel(), a.device.index):
+        # the plain call: a CUDA tensor on the current device, through the cached slot (a failed fast
+        # call wrote nothing: the general path below reruns it and raises / switches engines)
+        dev = a.device.index
+        if dev == torch.cuda.current_device() and _sort_device_fast(a, a.numel(), dev):
             return
+    _k_sort_general(a, counts)
+
+
+@_on_input_device
+def _k_sort_general(a: ArrayLike, counts: Optional[OpCounts] = None) -> None:
     flags = _lib.KS_FLAG_COUNTS if counts is not None else 0
     h = _host_view(a)
     if h is not None:   # host tensor / ndarray: copy in, sort, copy back with one synchronisation
