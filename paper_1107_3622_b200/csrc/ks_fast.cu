@@ -148,7 +148,7 @@ __device__ __forceinline__ void tl_rec(int kernel, int kind, long long len, unsi
 #define KS_SEG_FEED 1     // small-segment sorters: next item claimed / fetched / prefetched without stalls
 #endif
 #ifndef KS_SINGLE_MIN_N
-#define KS_SINGLE_MIN_N 8000000   // class-1 lists of inputs this large go to the single-buffer sorter (class 3)
+#define KS_SINGLE_MIN_N 5000000   // class-1 lists of inputs this large go to the single-buffer sorter (class 3), chained, draining class 0 (smaller single arrays: k_small)
 #endif
 #ifndef KS_MINB4
 #define KS_MINB4 8        // class 4 = class 0's keys by a single-buffer sorter (large inputs)
