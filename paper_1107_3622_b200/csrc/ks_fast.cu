@@ -4260,9 +4260,10 @@ static std::atomic<int> g_dloop_broken{0};   // a failed device-loop capture: gr
 static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 
 // Staged scatter tiles per SM in one pass.  A tile costs ~3-4 us of fixed work
-// (class table, scan, one bulk copy per gap run), so one small array gets one
-// tile per SM (1M keys: 489 tiles of 2K keys -> 140 of 7K); large arrays and
-// batches keep KS_STAGE_ITEMS_PER_SM (tile capacity kStageMax keys).
+// (class table, scan, one bulk copy per gap run), so one array gets as few
+// tiles per SM as its size allows (tile capacity kStageMax keys: 1 below 2.4M
+// keys, 2 below 4.8M, 3 below 7.4M -- 5.5M keys -5%, 6M -4%, 7M -1% against 4);
+// larger arrays and batches keep KS_STAGE_ITEMS_PER_SM.
 #ifndef KS_TO_LEAF
 #define KS_TO_LEAF 0   // measured: 1M +10%, 2M -3% (stragglers: groups up to 2x n / SMs keys); off
 #endif
@@ -4291,7 +4292,7 @@ static bool device_loop_ok() { return g_dloop_broken.load() == 0; }
 #define KS_IPSM2_MAX_N 4800000
 #endif
 #ifndef KS_IPSM3_MAX_N
-#define KS_IPSM3_MAX_N 0
+#define KS_IPSM3_MAX_N 7400000
 #endif
 static int stage_items_per_sm(long long n, bool batch)
 {

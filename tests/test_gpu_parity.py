@@ -530,9 +530,9 @@ def test_sizes_around_engine_limits():
         assert same_bits(host(t), np.sort(a)), n
 
 
-@pytest.mark.parametrize("n", [2_399_999, 2_400_001, 4_799_999, 4_800_001, 5_000_337])
+@pytest.mark.parametrize("n", [2_399_999, 2_400_001, 4_799_999, 4_800_001, 5_000_337, 7_399_999, 7_400_001])
 def test_sizes_around_tile_count_thresholds(n):
-    """One array gets 1 / 2 / 4 staged-scatter tiles per SM by its size (stage_items_per_sm in
+    """One array gets 1 / 2 / 3 / 4 staged-scatter tiles per SM by its size (stage_items_per_sm in
     ks_fast.cu): sizes on both sides of each switch, uniform keys and a skewed distribution
     (chunks at the tile capacity, multi-level passes), sorted twice (direct launch, then the graph)."""
     rng = np.random.default_rng(n)
