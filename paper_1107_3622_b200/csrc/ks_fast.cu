@@ -1809,6 +1809,12 @@ __global__ void __launch_bounds__(kScat2Threads, 1) k_scatter2(const Seg *segs, 
         }
 #endif
 #if KS_SCAT_TMA
+        // a tile without a single gap key (all its keys equal pivots: few distinct values)
+        // has nothing to move -- its keys and classes are not even read
+        if (tot == 2u * (unsigned)kScat2Threads) {
+            have = -1;
+            continue;
+        }
         // the previous tile's bulk copies have read the buffer (they overlapped this tile's table)
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 #endif
