@@ -80,7 +80,10 @@ constexpr int kKeysPerPivotLocal = KS_LOCAL_KPP;   // local partitions (children
 // pass so that a one-segment pass gives every CTA of the pass grid one chunk;
 // passes over several segments keep chunks <= kChunk (a segment's last chunk
 // is short, so long chunks would unbalance them)
-constexpr int kChunk = 16384;
+#ifndef KS_CHUNK
+#define KS_CHUNK 16384
+#endif
+constexpr int kChunk = KS_CHUNK;
 #ifndef KS_CHUNK_MIN
 #define KS_CHUNK_MIN 2048
 #endif
